@@ -1,0 +1,378 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 3DES-ECB engine (BASELINE.json metric:
+"3DES-ECB encrypt GB/s (1 and 8 B200) and % of LOP3-issue roofline").
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one pass of the hot path over one batch: ECB-encrypt the
+rank's 1 GiB shard (134,217,728 blocks; BASELINE configs[1], "encrypt 1 GB
+device-resident") with the bench key of the reference harness
+(bench.cpp:15-16).  Under torchrun each rank (one GPU) owns its own 1 GiB
+block range of one global stream (weak scaling, no data-path collective;
+the only collectives are the timing barrier and the max-over-ranks).
+
+value  = whole-job GB/s (decimal) from CUDA events on the launch stream,
+         inputs resident in HBM (1 GiB per step > 126 MB L2, so no flush);
+e2e    = the same metric through the C ABI's host-buffer entry
+         (t3des_cu_ecb_host: pinned H2D -> kernel -> D2H inside the timing);
+roofline = the LOP3-issue roofline of SURVEY.md §8d: W_alg = 402 lane-ops
+         per block; peak = SMs x 64 lane-ops/clk x sm_max_mhz.
+cpu_baseline = the reference's own OpenMP CPU path (oracle/_ref, Backend::
+         Threaded, all host threads) on a bounded sample, rank 0 at N=1.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BENCH_KEY = "133457799BBCDFF10E329232EA6D0D737CA110454A1A6E57"
+METRIC = "3DES-ECB encrypt GB/s (1 and 8 B200) and % of LOP3-issue roofline"
+W_ALG = 402.0  # LOP3 lane-ops per block (fixed yardstick)
+ALU_LANES_PER_CLK_PER_SM = 64
+SEED = 0x3DE5C0DE
+
+
+def env_int(name: str, default: int) -> int:
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def measured_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+        self.t = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            if self.t:
+                self.t.join(timeout=2)
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx.append(float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm_sorted = sorted(sm)
+        return {"sm_mhz": sm_sorted[len(sm_sorted) // 2], "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_reference_arm(nbytes_target_s: float = 12.0):
+    """Time the reference's own CPU implementation of the path: oracle/_ref
+    (Backend::Threaded, OpenMP, all host threads) when it was compiled, else
+    the C restatement (oracle/liboracle.so, fused route, OpenMP).  Returns
+    (GB/s, cores, kind, sample description)."""
+    import numpy as np
+
+    from tests.oracle_util import Oracle
+
+    o = Oracle.load()
+    s = o.schedule_hex(BENCH_KEY)
+    cores = os.cpu_count() or 1
+
+    def run(buf, out):
+        if o.ref is not None:
+            rc = o.ref.ref_ecb(buf.ctypes.data, out.ctypes.data, buf.nbytes, s, 0, 1, 0, 0, 0)
+        else:
+            rc = o.lib.oracle_ecb(buf.ctypes.data, out.ctypes.data, buf.nbytes, s, 0, 1, 0)
+        assert rc == 0
+
+    kind = "reference" if o.ref is not None else "port"
+    if o.ref is not None:
+        cores = int(o.ref.ref_resolve_workers(0))
+    probe = o.payload(8 << 20)
+    out = np.empty_like(probe)
+    run(probe, out)  # warm-up
+    t0 = time.perf_counter()
+    run(probe, out)
+    rate = probe.nbytes / max(time.perf_counter() - t0, 1e-9)
+    sample = int(min(1 << 30, max(8 << 20, rate * nbytes_target_s / 2))) // 8 * 8
+    buf = o.payload(sample)
+    out = np.empty_like(buf)
+    best = None
+    for _ in range(2):
+        t0 = time.perf_counter()
+        run(buf, out)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    gbs = sample / best / 1e9
+    desc = (f"encrypt of {sample >> 20} MiB make_payload(seed 0x3DE5C0DE) with the bench key, "
+            f"{'reference encrypt_batch Backend::Threaded' if kind == 'reference' else 'oracle port'}, "
+            f"chunk 131072 / work_group 256, {cores} threads, min of 2")
+    return gbs, cores, kind, desc
+
+
+def run_reference_impl(args, rank: int, world: int) -> None:
+    if rank != 0:
+        return
+    import numpy as np  # noqa: F401
+
+    per_step = []
+    gbs = cores = kind = desc = None
+    for i in range(args.warmup + args.steps):
+        g, cores, kind, desc = cpu_reference_arm(nbytes_target_s=4.0)
+        if i >= args.warmup:
+            per_step.append(g)
+    gbs = sorted(per_step)[len(per_step) // 2]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(gbs, 4), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": workload_config(args, world),
+        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": cores, "kind": kind,
+                         "sample": desc + " per step (median of steps)"},
+        "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, world: int) -> dict:
+    return {
+        "workload": f"3DES-ECB encrypt {args.gib} GiB device-resident per GPU (BASELINE configs[1]); "
+                    f"N>1: block-range shards of one stream (configs[3])",
+        "key": BENCH_KEY, "keying_option": 1,
+        "blocks_per_gpu": (args.gib << 30) // 8, "global_blocks": world * ((args.gib << 30) // 8),
+        "variant": args.variant, "payload": "splitmix64(seed ^ block index) generated on device",
+        "l2_policy": "inputs larger than L2 (1 GiB per step vs 126 MB L2), no flush",
+        "parallelism": f"block-range shards x{world}, no data-path collective",
+    }
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--variant", choices=["bitslice", "sptable"], default="bitslice")
+    ap.add_argument("--gib", type=int, default=1, help="GiB per GPU per step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-variants", action="store_true")
+    ap.add_argument("--traffic-bytes", type=float, default=None,
+                    help="dram bytes per launch from an ncu --set full capture (else read profiles/)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        run_reference_impl(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1305_4376_b200 as t3
+    from paper_1305_4376_b200 import _native as N
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    e = t3.Engine(local)
+    ts = t3.triple_schedule(t3.parse_hex_key(BENCH_KEY))
+    e.set_schedule(ts)
+    e.set_variant(N.VARIANT_SPTABLE if args.variant == "sptable" else N.VARIANT_BITSLICE)
+    nblocks = (args.gib << 30) // 8
+    nbytes = 8 * nblocks
+    first_block = rank * nblocks
+    stream = torch.cuda.Stream()
+    sp = stream.cuda_stream
+    src = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    dst = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    with torch.cuda.stream(stream):
+        e.fill_splitmix(src.data_ptr(), first_block, nblocks, SEED, sp)
+    torch.cuda.synchronize()
+
+    # sampled correctness gate before timing (bit-exact vs the CPU oracle)
+    from tests.oracle_util import Oracle
+    import numpy as np
+
+    orc = Oracle.load()
+    e.ecb_device(0, src.data_ptr(), dst.data_ptr(), nbytes, sp)
+    torch.cuda.synchronize()
+    idx = torch.arange(0, nblocks, max(1, nblocks // 4096), device="cuda")
+    got = dst.view(torch.int64)[idx].cpu().numpy().view(np.uint8)
+    inp = src.view(torch.int64)[idx].cpu().numpy().view(np.uint8)
+    parity_ok = bool(np.array_equal(got, orc.ecb(inp, orc.schedule_hex(BENCH_KEY), 0)))
+
+    for _ in range(args.warmup):
+        e.ecb_device(0, src.data_ptr(), dst.data_ptr(), nbytes, sp)
+    barrier()
+    l0 = e.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            e.ecb_device(0, src.data_ptr(), dst.data_ptr(), nbytes, sp)
+        ev1.record(stream)
+        barrier()
+    launches = e.launch_count() - l0
+    ms_total = ev0.elapsed_time(ev1)
+    ms_step = max_over_ranks(ms_total / args.steps)
+    gbs = world * nbytes / (ms_step * 1e-3) / 1e9
+    blocks_per_s = world * nblocks / (ms_step * 1e-3)
+    clocks = clk.summary()
+
+    peaks = measured_peaks()
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    fmax = float(peaks.get("sm_max_mhz", 1965.0))
+    peak_tlops = sms * ALU_LANES_PER_CLK_PER_SM * fmax * 1e6 / 1e12
+    per_gpu_bps = nblocks / (ms_step * 1e-3)
+    achieved = per_gpu_bps * W_ALG / 1e12
+    traffic = args.traffic_bytes
+    if traffic is None:
+        try:
+            with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+                traffic = json.load(f).get(args.variant)
+        except Exception:
+            traffic = None
+    hbm_peak = float(peaks.get("hbm_gbs", 6553.3))
+    roofline = {
+        "bound": "alu", "achieved": round(achieved, 4), "peak": round(peak_tlops, 4), "unit": "Tlop3/s",
+        "frac": round(achieved / peak_tlops, 4), "traffic": traffic,
+        "kernel_ms": round(ms_step, 4),
+        "peak_source": f"{sms} SMs x {ALU_LANES_PER_CLK_PER_SM} ALU lanes/clk x sm_max_mhz {fmax:.0f} "
+                       f"({'MEASURED_PEAKS.json' if 'sm_max_mhz' in peaks else 'fallback'})",
+        "frac_at_run_clock": (round(achieved / (sms * 64 * clocks["sm_mhz"] * 1e6 / 1e12), 4)
+                              if clocks.get("sm_mhz") else None),
+        "w_alg_lane_ops_per_block": W_ALG,
+        "hbm": {"achieved_gbs": round(per_gpu_bps * 16 / 1e9, 2), "peak_gbs": hbm_peak,
+                "frac": round(per_gpu_bps * 16 / 1e9 / hbm_peak, 4), "bytes_per_block": 16},
+    }
+
+    line = {
+        "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": workload_config(args, world),
+        "roofline": roofline, "clocks": clocks, "gpu_launches": int(launches),
+        "parity_sampled_vs_oracle": parity_ok,
+    }
+
+    # secondary variant (north star: bitsliced vs SP-table, ncu picks)
+    if not args.no_variants:
+        other = "sptable" if args.variant == "bitslice" else "bitslice"
+        e.set_variant(N.VARIANT_SPTABLE if other == "sptable" else N.VARIANT_BITSLICE)
+        for _ in range(2):
+            e.ecb_device(0, src.data_ptr(), dst.data_ptr(), nbytes, sp)
+        barrier()
+        k2 = max(3, args.steps // 4)
+        ev0.record(stream)
+        for _ in range(k2):
+            e.ecb_device(0, src.data_ptr(), dst.data_ptr(), nbytes, sp)
+        ev1.record(stream)
+        barrier()
+        ms2 = max_over_ranks(ev0.elapsed_time(ev1) / k2)
+        line["variants"] = {args.variant: round(gbs, 3), other: round(world * nbytes / (ms2 * 1e-3) / 1e9, 3)}
+        e.set_variant(N.VARIANT_SPTABLE if args.variant == "sptable" else N.VARIANT_BITSLICE)
+
+    del dst
+    torch.cuda.empty_cache()
+
+    # end to end through the C ABI host entry (pinned H2D + kernel + D2H)
+    if not args.no_e2e:
+        host = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+        host.copy_(src.cpu())
+        del src
+        torch.cuda.empty_cache()
+        e.ecb_host(0, host.data_ptr(), host.data_ptr(), nbytes)  # warm (allocates staging)
+        k3 = max(3, min(args.steps, 5))
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(k3):
+            e.ecb_host(0, host.data_ptr(), host.data_ptr(), nbytes)
+        dt = max_over_ranks((time.perf_counter() - t0) / k3)
+        line["e2e"] = {"value": round(world * nbytes / dt / 1e9, 3), "unit": "GB/s",
+                       "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+                       "path": "t3des_cu_ecb_host, pinned host buffer, 64 MiB chunks over 3 streams",
+                       "steps": k3}
+    else:
+        line["e2e"] = None
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        g, cores, kind, desc = cpu_reference_arm()
+        line["cpu_baseline"] = {"value": round(g, 4), "unit": "GB/s", "cores": cores, "kind": kind, "sample": desc}
+
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    e.close()
+
+
+if __name__ == "__main__":
+    main()

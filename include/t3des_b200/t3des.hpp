@@ -1,0 +1,104 @@
+// C++ host API of the B200 3DES-ECB engine, mirroring the reference's hot
+// path API so C++ callers switch by changing the include and the link line:
+//
+//   reference (/root/reference/proj/include/t3des)    this header
+//   tdes.hpp:14-23  KeyingOption, TripleKey          same names
+//   tdes.hpp:32     parse_hex_key                    same signature
+//   des.hpp:33-35   key_schedule                     same signature
+//   tdes.hpp:36-42  TripleSchedule, triple_schedule  same layout (pass-major)
+//   des.hpp:30-31   load_block / store_block         same (big-endian)
+//   dispatch.hpp:19-30  Backend, DispatchConfig      + Backend::Cuda (default)
+//   dispatch.hpp:39-42  plan_dispatch, ChunkSpan     same
+//   dispatch.hpp:64-69  encrypt_batch/decrypt_batch  same signatures
+//   dispatch.hpp:44-47, tdes.hpp:25-28  InputLengthError, KeyFormatError
+//
+// Backend::Cuda sends the whole batch through the C ABI (t3des_cu.h) in
+// one call; there is no CPU cipher in this library (ScalarReference and
+// Threaded are the reference's own CPU backends and throw here).
+#pragma once
+
+#include <array>
+#include <cstddef>
+#include <cstdint>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <vector>
+
+namespace t3des {
+
+using Block = std::uint64_t;
+using RoundKeySet = std::array<std::uint64_t, 16>;
+
+struct DesKey {
+    std::uint64_t raw = 0;
+};
+
+enum class KeyingOption { Option1, Option2, Option3 };
+
+struct TripleKey {
+    DesKey k1, k2, k3;
+    KeyingOption option = KeyingOption::Option1;
+};
+
+class KeyFormatError : public std::runtime_error {
+  public:
+    using std::runtime_error::runtime_error;
+};
+
+class InputLengthError : public std::runtime_error {
+  public:
+    using std::runtime_error::runtime_error;
+};
+
+// CUDA runtime / device failures (no device is an error, never a fallback).
+class CudaError : public std::runtime_error {
+  public:
+    CudaError(const std::string& what, int code) : std::runtime_error(what), status(code) {}
+    int status;
+};
+
+TripleKey parse_hex_key(std::string_view hex);
+RoundKeySet key_schedule(DesKey key);
+
+struct TripleSchedule {
+    RoundKeySet pass1, pass2, pass3;
+};
+TripleSchedule triple_schedule(const TripleKey& key);
+
+Block load_block(std::span<const std::uint8_t, 8> bytes);
+void store_block(Block b, std::span<std::uint8_t, 8> out);
+
+enum class Backend {
+    ScalarReference,  // reference CPU oracle — not in this library
+    Threaded,         // reference OpenMP backend — not in this library
+    NoOpCopy,         // copy only (timing instrumentation), as in the reference
+    Cuda,             // B200 kernels through the C ABI
+};
+
+struct DispatchConfig {
+    std::size_t chunk_blocks = 131072;  // reference meaning; the CUDA backend sends the
+                                        // whole batch per call (blocks per launch only
+                                        // when gpu_chunked is set)
+    std::size_t work_group = 256;       // CUDA: threads per CTA hint (used when gpu_chunked)
+    unsigned workers = 0;               // CUDA: number of GPUs (0 = 1, device `device`)
+    Backend backend = Backend::Cuda;
+    int device = 0;                     // first CUDA device
+    int variant = 0;                    // 0 bitsliced (default), 1 SP-table
+    bool gpu_chunked = false;           // apply chunk_blocks/work_group to launches
+};
+
+struct ChunkSpan {
+    std::size_t offset;  // in blocks
+    std::size_t length;  // in blocks
+};
+
+std::vector<ChunkSpan> plan_dispatch(std::size_t total_blocks, const DispatchConfig& cfg);
+
+void encrypt_batch(std::span<const std::uint8_t> in, std::span<std::uint8_t> out,
+                   const TripleSchedule& ts, const DispatchConfig& cfg);
+void decrypt_batch(std::span<const std::uint8_t> in, std::span<std::uint8_t> out,
+                   const TripleSchedule& ts, const DispatchConfig& cfg);
+
+}  // namespace t3des

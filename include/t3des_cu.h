@@ -1,0 +1,139 @@
+/*
+ * t3des_cu.h — C ABI of the B200-native 3DES-ECB engine
+ * (libt3des_b200.so, built from paper_1305_4376_b200/csrc).
+ *
+ * This is the drop-in boundary for the reference's hot path.  The
+ * reference (/root/reference/proj, "t3des") exposes a C++ API; its batch
+ * entry points are
+ *     void encrypt_batch(std::span<const uint8_t> in, std::span<uint8_t> out,
+ *                        const TripleSchedule&, const DispatchConfig&);
+ *     void decrypt_batch(...);                  (include/t3des/dispatch.hpp:64-69)
+ * dispatched per chunk to a Backend in run_chunk (src/dispatch.cpp:60-86).
+ * The engine plugs in as a new Backend::Cuda routed from run_batch
+ * (src/dispatch.cpp:105) to t3des_cu_ecb_host — see INTEGRATION.md.
+ *
+ * Conventions
+ *   - plain pointers and sizes, no C++ or torch types;
+ *   - every function returns an int status (T3DES_CU_OK = 0); nothing
+ *     throws across the ABI; t3des_cu_strerror() maps codes to text;
+ *   - no CPU fallback: without a usable sm_100 device the device-facing
+ *     calls fail with T3DES_CU_ERR_NO_DEVICE / T3DES_CU_ERR_CUDA;
+ *   - a context is used from one submitting thread at a time
+ *     (reference SPEC.md:233: "safe to use from one submitting context").
+ */
+#ifndef T3DES_CU_H
+#define T3DES_CU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes.  The C++ layer maps 1-2 to InputLengthError
+ * (dispatch.hpp:44-47) and 3 to KeyFormatError (tdes.hpp:25-28). */
+#define T3DES_CU_OK 0
+#define T3DES_CU_ERR_LENGTH 1      /* byte length not a multiple of 8       */
+#define T3DES_CU_ERR_OVERLAP 2     /* in/out partially overlap              */
+#define T3DES_CU_ERR_KEY 3         /* hex key: bad length or character      */
+#define T3DES_CU_ERR_ARG 4         /* null pointer, bad enum, bad size      */
+#define T3DES_CU_ERR_NO_DEVICE 5   /* no CUDA device / not sm_100           */
+#define T3DES_CU_ERR_CUDA 6        /* a CUDA runtime call failed            */
+#define T3DES_CU_ERR_NO_SCHEDULE 7 /* t3des_cu_set_schedule not called yet  */
+
+#define T3DES_CU_ENCRYPT 0
+#define T3DES_CU_DECRYPT 1
+
+#define T3DES_CU_VARIANT_BITSLICE 0 /* bitsliced lop3 kernel (default)  */
+#define T3DES_CU_VARIANT_SPTABLE 1  /* shared-memory SP-table kernel    */
+
+typedef struct t3des_cu_ctx t3des_cu_ctx;
+
+/* Library version (major*10000 + minor*100 + patch). */
+int t3des_cu_version(void);
+const char* t3des_cu_strerror(int code);
+
+/* ---- keying (host only, no device needed) ------------------------------ */
+
+/* Replaces parse_hex_key (tdes.hpp:32; tdes.cpp:32-59): 48/32/16 hex chars
+ * -> keying option 1/2/3 (written to *option) and keys k1,k2,k3 (k3 = k1
+ * for option 2; all equal for option 3).  T3DES_CU_ERR_KEY on bad input. */
+int t3des_cu_parse_hex_key(const char* hex, size_t len, uint64_t keys[3], int* option);
+
+/* Replaces triple_schedule (tdes.hpp:42; tdes.cpp:84-87): 48 subkeys,
+ * pass-major (16 for k1, then k2, then k3) — exactly the memory of the
+ * reference's TripleSchedule {pass1, pass2, pass3} (tdes.hpp:38-40). */
+int t3des_cu_triple_schedule(const uint64_t keys[3], uint64_t sub48[48]);
+
+/* ---- contexts ------------------------------------------------------------ */
+
+int t3des_cu_device_count(int* count);
+
+/* One context per device; owns its streams and staging buffers. */
+int t3des_cu_create(int device, t3des_cu_ctx** out);
+int t3des_cu_destroy(t3des_cu_ctx* ctx);
+
+/* Install the 48-subkey schedule (pass-major, as above).  The host
+ * flattens it once into the encrypt and decrypt execution sequences
+ * (tdes.cpp:177-185) and the kernels' constant tables; no device traffic. */
+int t3des_cu_set_schedule(t3des_cu_ctx* ctx, const uint64_t sub48[48]);
+
+/* T3DES_CU_VARIANT_*; default BITSLICE. */
+int t3des_cu_set_variant(t3des_cu_ctx* ctx, int variant);
+
+/* Launch shaping, the GPU reading of DispatchConfig (dispatch.hpp:25-30):
+ * chunk_blocks = blocks per kernel launch (0 = whole batch in one launch,
+ * the default), work_group = threads per CTA (0 = kernel default).  Only
+ * for Table I/II-style sweeps; results never depend on them. */
+int t3des_cu_set_launch(t3des_cu_ctx* ctx, size_t chunk_blocks, int work_group);
+
+/* ---- ECB batch ------------------------------------------------------------ */
+
+/* Device-resident batch: din/dout are device pointers on the context's
+ * device, len is in bytes.  Asynchronous on `stream` (a cudaStream_t; NULL
+ * = legacy default stream).  in == out (in place) is allowed, partial
+ * overlap is rejected, len == 0 is a no-op (dispatch.cpp:91-104,215). */
+int t3des_cu_ecb_device(t3des_cu_ctx* ctx, int direction, const void* din, void* dout,
+                        size_t len, void* stream);
+
+/* Host buffers, end to end: chunked H2D -> kernel -> D2H pipelined over
+ * three streams; returns when `out` holds the result.  This is the entry
+ * a Backend::Cuda branch of run_batch calls (same contract as
+ * encrypt_batch/decrypt_batch).  Pinned buffers (t3des_cu_host_alloc)
+ * give full PCIe overlap; pageable buffers work, more slowly. */
+int t3des_cu_ecb_host(t3des_cu_ctx* ctx, int direction, const uint8_t* in, uint8_t* out,
+                      size_t len);
+
+/* Host buffers sharded by contiguous block ranges (multiples of 1024
+ * blocks) over `ndev` devices, one host thread and context per device; no
+ * collective.  Blocks are independent, so the result equals
+ * the single-device result. */
+int t3des_cu_ecb_multi(const int* devices, int ndev, const uint64_t sub48[48], int direction,
+                       const uint8_t* in, uint8_t* out, size_t len);
+
+/* ---- utilities --------------------------------------------------------- */
+
+/* Pinned host memory for t3des_cu_ecb_host. */
+int t3des_cu_host_alloc(size_t bytes, void** out);
+int t3des_cu_host_free(void* p);
+
+/* Device payload generator for inputs larger than host RAM: block
+ * (first_block + i) = splitmix64(seed ^ (first_block + i)), big-endian. */
+int t3des_cu_fill_splitmix(t3des_cu_ctx* ctx, void* dptr, uint64_t first_block, size_t nblocks,
+                           uint64_t seed, void* stream);
+
+/* Shard-additive, order-sensitive checksum of nblocks device blocks whose
+ * global index starts at first_block; synchronous, result in *out. */
+int t3des_cu_checksum(t3des_cu_ctx* ctx, const void* dptr, uint64_t first_block, size_t nblocks,
+                      uint64_t* out);
+
+/* Number of cipher kernels this context has launched (for bench.py's
+ * gpu_launches count). */
+int t3des_cu_launch_count(t3des_cu_ctx* ctx, uint64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* T3DES_CU_H */

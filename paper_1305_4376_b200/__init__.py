@@ -1,0 +1,36 @@
+"""B200-native 3DES-ECB engine (arxiv 1305.4376 hot path, rebuilt for sm_100a).
+
+Host API mirroring the reference's t3des API; the cipher runs only in the
+CUDA kernels of libt3des_b200.so.
+"""
+from ._native import (  # noqa: F401
+    DECRYPT,
+    ENCRYPT,
+    VARIANT_BITSLICE,
+    VARIANT_SPTABLE,
+    EngineUnavailable,
+    LIB_PATH,
+)
+from .api import (  # noqa: F401
+    Backend,
+    ChunkSpan,
+    CudaError,
+    DesKey,
+    DispatchConfig,
+    Engine,
+    InputLengthError,
+    KeyFormatError,
+    KeyingOption,
+    TripleKey,
+    TripleSchedule,
+    decrypt_batch,
+    encrypt_batch,
+    engine,
+    key_schedule,
+    load_block,
+    parse_hex_key,
+    plan_dispatch,
+    store_block,
+    to_hex,
+    triple_schedule,
+)

@@ -1,0 +1,402 @@
+// C ABI of the B200 3DES-ECB engine (declared in include/t3des_cu.h).
+//
+// Owns: device selection, per-context streams and staging buffers, the
+// host-flattened key tables, kernel launch shaping, the pipelined
+// host-buffer path and the multi-GPU block-range sharding.  No exception
+// crosses this boundary and there is no CPU fallback.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <thread>
+#include <vector>
+
+#include "kernels.cuh"
+#include "schedule.hpp"
+#include "t3des_cu.h"
+
+struct t3des_cu_ctx {
+    int device = 0;
+    int sms = 0;
+    int bs_occ = 1;  // CTAs per SM for the bitsliced kernel
+    int sp_occ = 1;
+    bool have_schedule = false;
+    int variant = T3DES_CU_VARIANT_BITSLICE;
+    std::size_t chunk_blocks = 0;
+    int work_group = 0;
+    T3BsTable bs[2];
+    T3SpKeyParam sp[2];
+    std::uint32_t* d_sp = nullptr;  // 8x64 fused S/P table (2 KiB)
+    unsigned long long* d_acc = nullptr;
+    cudaStream_t st[3] = {nullptr, nullptr, nullptr};
+    std::uint8_t* buf[3] = {nullptr, nullptr, nullptr};
+    std::size_t buf_bytes = 0;
+    std::uint64_t launches = 0;
+};
+
+namespace {
+
+constexpr std::size_t kHostChunkBytes = std::size_t(64) << 20;  // per pipeline stage
+constexpr int kSpSmemBytes = 8 * 64 * 32 * 4;                   // 64 KiB
+
+// Restores the caller's current device on scope exit.
+struct DeviceScope {
+    int prev = -1;
+    explicit DeviceScope(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        cudaSetDevice(dev);
+    }
+    ~DeviceScope() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+#define T3_CK(call)                                   \
+    do {                                              \
+        if ((call) != cudaSuccess) {                  \
+            (void)cudaGetLastError();                 \
+            return T3DES_CU_ERR_CUDA;                 \
+        }                                             \
+    } while (0)
+
+bool partial_overlap(const void* a, const void* b, std::size_t len) {
+    const auto* x = static_cast<const std::uint8_t*>(a);
+    const auto* y = static_cast<const std::uint8_t*>(b);
+    return x != y && y < x + len && y + len > x;
+}
+
+int launch_bitslice(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8_t* out,
+                    std::uint64_t nblocks, cudaStream_t s) {
+    const std::uint64_t full = nblocks / T3_TILE_BLOCKS;
+    const bool tail = (nblocks % T3_TILE_BLOCKS) != 0;
+    const int threads = c->work_group > 0 ? c->work_group : T3_BS_THREADS;
+    if (full) {
+        const std::uint64_t warps_per_cta = std::uint64_t(threads) / 32;
+        std::uint64_t grid = (full + warps_per_cta - 1) / warps_per_cta;
+        const std::uint64_t cap = std::uint64_t(c->sms) * std::uint64_t(c->bs_occ) *
+                                  (T3_BS_THREADS / 32) / warps_per_cta;
+        grid = std::min<std::uint64_t>(grid, std::max<std::uint64_t>(cap, 1));
+        const bool vec4 = ((reinterpret_cast<std::uintptr_t>(in) |
+                            reinterpret_cast<std::uintptr_t>(out)) & 15u) == 0;
+        if (vec4)
+            t3_bs_kernel<4, false><<<unsigned(grid), threads, 0, s>>>(in, out, 0, full, nblocks, c->bs[dir]);
+        else
+            t3_bs_kernel<2, false><<<unsigned(grid), threads, 0, s>>>(in, out, 0, full, nblocks, c->bs[dir]);
+        T3_CK(cudaGetLastError());
+        ++c->launches;
+    }
+    if (tail) {
+        t3_bs_kernel<2, true><<<1, 32, 0, s>>>(in, out, full, 1, nblocks, c->bs[dir]);
+        T3_CK(cudaGetLastError());
+        ++c->launches;
+    }
+    return T3DES_CU_OK;
+}
+
+int launch_sptable(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8_t* out,
+                   std::uint64_t nblocks, cudaStream_t s) {
+    const int threads = c->work_group > 0 ? c->work_group : T3_SP_THREADS;
+    std::uint64_t grid = (nblocks + threads - 1) / threads;
+    grid = std::min<std::uint64_t>(grid, std::uint64_t(c->sms) * std::uint64_t(c->sp_occ));
+    t3_sp_kernel<<<unsigned(std::max<std::uint64_t>(grid, 1)), threads, kSpSmemBytes, s>>>(
+        reinterpret_cast<const uint2*>(in), reinterpret_cast<uint2*>(out), nblocks, c->d_sp, c->sp[dir]);
+    T3_CK(cudaGetLastError());
+    ++c->launches;
+    return T3DES_CU_OK;
+}
+
+// Transform nblocks device blocks (in may equal out), honouring the
+// context's chunk_blocks (blocks per launch).
+int run_device(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8_t* out,
+               std::uint64_t nblocks, cudaStream_t s) {
+    if (nblocks == 0) return T3DES_CU_OK;
+    const std::uint64_t step = c->chunk_blocks ? c->chunk_blocks : nblocks;
+    for (std::uint64_t off = 0; off < nblocks; off += step) {
+        const std::uint64_t n = std::min(step, nblocks - off);
+        const int rc = c->variant == T3DES_CU_VARIANT_SPTABLE
+                           ? launch_sptable(c, dir, in + 8 * off, out + 8 * off, n, s)
+                           : launch_bitslice(c, dir, in + 8 * off, out + 8 * off, n, s);
+        if (rc) return rc;
+    }
+    return T3DES_CU_OK;
+}
+
+int check_batch(t3des_cu_ctx* c, int dir, const void* in, const void* out, std::size_t len) {
+    if (!c || (dir != T3DES_CU_ENCRYPT && dir != T3DES_CU_DECRYPT)) return T3DES_CU_ERR_ARG;
+    if (len % 8) return T3DES_CU_ERR_LENGTH;
+    if (len && (!in || !out)) return T3DES_CU_ERR_ARG;
+    if (partial_overlap(in, out, len)) return T3DES_CU_ERR_OVERLAP;
+    if (!c->have_schedule) return T3DES_CU_ERR_NO_SCHEDULE;
+    return T3DES_CU_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int t3des_cu_version(void) { return 1 * 10000 + 0 * 100 + 0; }
+
+const char* t3des_cu_strerror(int code) {
+    switch (code) {
+        case T3DES_CU_OK: return "ok";
+        case T3DES_CU_ERR_LENGTH: return "batch length is not a multiple of 8 bytes";
+        case T3DES_CU_ERR_OVERLAP: return "partially overlapping buffers";
+        case T3DES_CU_ERR_KEY: return "key must be 16, 32 or 48 hex characters";
+        case T3DES_CU_ERR_ARG: return "invalid argument";
+        case T3DES_CU_ERR_NO_DEVICE: return "no usable sm_100 CUDA device";
+        case T3DES_CU_ERR_CUDA: return "CUDA runtime error";
+        case T3DES_CU_ERR_NO_SCHEDULE: return "no key schedule installed";
+        default: return "unknown error";
+    }
+}
+
+int t3des_cu_parse_hex_key(const char* hex, std::size_t len, std::uint64_t keys[3], int* option) {
+    if (!hex || !keys) return T3DES_CU_ERR_ARG;
+    const int opt = t3b::parse_hex_key(hex, len, keys);
+    if (opt < 0) return T3DES_CU_ERR_KEY;
+    if (option) *option = opt;
+    return T3DES_CU_OK;
+}
+
+int t3des_cu_triple_schedule(const std::uint64_t keys[3], std::uint64_t sub48[48]) {
+    if (!keys || !sub48) return T3DES_CU_ERR_ARG;
+    t3b::triple_schedule(keys, sub48);
+    return T3DES_CU_OK;
+}
+
+int t3des_cu_device_count(int* count) {
+    if (!count) return T3DES_CU_ERR_ARG;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        (void)cudaGetLastError();
+        n = 0;
+    }
+    *count = n;
+    return T3DES_CU_OK;
+}
+
+int t3des_cu_create(int device, t3des_cu_ctx** out) {
+    if (!out) return T3DES_CU_ERR_ARG;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) {
+        (void)cudaGetLastError();
+        return T3DES_CU_ERR_NO_DEVICE;
+    }
+    cudaDeviceProp prop;
+    T3_CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) return T3DES_CU_ERR_NO_DEVICE;  // built for sm_100a only
+    DeviceScope scope(device);
+    auto* c = new (std::nothrow) t3des_cu_ctx();
+    if (!c) return T3DES_CU_ERR_ARG;
+    c->device = device;
+    c->sms = prop.multiProcessorCount;
+    int rc = T3DES_CU_OK;
+    do {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->bs_occ, t3_bs_kernel<4, false>,
+                                                          T3_BS_THREADS, 0) != cudaSuccess) {
+            rc = T3DES_CU_ERR_CUDA;
+            break;
+        }
+        if (cudaFuncSetAttribute(t3_sp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kSpSmemBytes) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->sp_occ, t3_sp_kernel, T3_SP_THREADS,
+                                                          kSpSmemBytes) != cudaSuccess) {
+            rc = T3DES_CU_ERR_CUDA;
+            break;
+        }
+        c->bs_occ = std::max(c->bs_occ, 1);
+        c->sp_occ = std::max(c->sp_occ, 1);
+        std::uint32_t sp[8][64];
+        t3b::build_sp_tables(sp);
+        if (cudaMalloc(&c->d_sp, sizeof sp) != cudaSuccess ||
+            cudaMemcpy(c->d_sp, sp, sizeof sp, cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMalloc(&c->d_acc, sizeof(unsigned long long)) != cudaSuccess) {
+            rc = T3DES_CU_ERR_CUDA;
+            break;
+        }
+        for (auto& s : c->st)
+            if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) rc = T3DES_CU_ERR_CUDA;
+    } while (false);
+    if (rc) {
+        (void)cudaGetLastError();
+        t3des_cu_destroy(c);
+        return rc;
+    }
+    *out = c;
+    return T3DES_CU_OK;
+}
+
+int t3des_cu_destroy(t3des_cu_ctx* c) {
+    if (!c) return T3DES_CU_ERR_ARG;
+    {
+        DeviceScope scope(c->device);
+        for (auto& s : c->st)
+            if (s) cudaStreamDestroy(s);
+        for (auto& b : c->buf)
+            if (b) cudaFree(b);
+        if (c->d_sp) cudaFree(c->d_sp);
+        if (c->d_acc) cudaFree(c->d_acc);
+        (void)cudaGetLastError();
+    }
+    delete c;
+    return T3DES_CU_OK;
+}
+
+int t3des_cu_set_schedule(t3des_cu_ctx* c, const std::uint64_t sub48[48]) {
+    if (!c || !sub48) return T3DES_CU_ERR_ARG;
+    for (int dir = 0; dir < 2; ++dir) {
+        std::uint64_t seq[48];
+        t3b::key_sequence(sub48, dir == T3DES_CU_DECRYPT, seq);
+        t3b::build_bitslice_table(seq, c->bs[dir]);
+        t3b::SpKeys k;
+        t3b::build_sp_keys(seq, k);
+        std::memcpy(c->sp[dir].k, k.k, sizeof k.k);
+    }
+    c->have_schedule = true;
+    return T3DES_CU_OK;
+}
+
+int t3des_cu_set_variant(t3des_cu_ctx* c, int variant) {
+    if (!c || (variant != T3DES_CU_VARIANT_BITSLICE && variant != T3DES_CU_VARIANT_SPTABLE))
+        return T3DES_CU_ERR_ARG;
+    c->variant = variant;
+    return T3DES_CU_OK;
+}
+
+int t3des_cu_set_launch(t3des_cu_ctx* c, std::size_t chunk_blocks, int work_group) {
+    if (!c || work_group < 0 || work_group > 1024 || (work_group % 32) != 0) return T3DES_CU_ERR_ARG;
+    if (work_group > T3_BS_THREADS && c->variant == T3DES_CU_VARIANT_BITSLICE) return T3DES_CU_ERR_ARG;
+    c->chunk_blocks = chunk_blocks;
+    c->work_group = work_group;
+    return T3DES_CU_OK;
+}
+
+int t3des_cu_ecb_device(t3des_cu_ctx* c, int dir, const void* din, void* dout, std::size_t len,
+                        void* stream) {
+    const int rc = check_batch(c, dir, din, dout, len);
+    if (rc) return rc;
+    if (!len) return T3DES_CU_OK;
+    DeviceScope scope(c->device);
+    return run_device(c, dir, static_cast<const std::uint8_t*>(din), static_cast<std::uint8_t*>(dout),
+                      len / 8, static_cast<cudaStream_t>(stream));
+}
+
+int t3des_cu_ecb_host(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8_t* out,
+                      std::size_t len) {
+    int rc = check_batch(c, dir, in, out, len);
+    if (rc) return rc;
+    if (!len) return T3DES_CU_OK;
+    DeviceScope scope(c->device);
+    const std::size_t chunk = std::min(len, kHostChunkBytes);
+    if (c->buf_bytes < chunk) {
+        for (auto& b : c->buf) {
+            if (b) cudaFree(b);
+            b = nullptr;
+        }
+        c->buf_bytes = 0;
+        for (auto& b : c->buf) T3_CK(cudaMalloc(&b, chunk));
+        c->buf_bytes = chunk;
+    }
+    std::size_t k = 0;
+    for (std::size_t off = 0; off < len; off += chunk, ++k) {
+        const std::size_t n = std::min(chunk, len - off);
+        cudaStream_t s = c->st[k % 3];
+        std::uint8_t* b = c->buf[k % 3];
+        T3_CK(cudaMemcpyAsync(b, in + off, n, cudaMemcpyHostToDevice, s));
+        rc = run_device(c, dir, b, b, n / 8, s);
+        if (rc) return rc;
+        T3_CK(cudaMemcpyAsync(out + off, b, n, cudaMemcpyDeviceToHost, s));
+    }
+    for (auto& s : c->st) T3_CK(cudaStreamSynchronize(s));
+    return T3DES_CU_OK;
+}
+
+int t3des_cu_ecb_multi(const int* devices, int ndev, const std::uint64_t sub48[48], int dir,
+                       const std::uint8_t* in, std::uint8_t* out, std::size_t len) {
+    if (!devices || ndev <= 0 || !sub48 || (dir != 0 && dir != 1)) return T3DES_CU_ERR_ARG;
+    if (len % 8) return T3DES_CU_ERR_LENGTH;
+    if (len && (!in || !out)) return T3DES_CU_ERR_ARG;
+    if (partial_overlap(in, out, len)) return T3DES_CU_ERR_OVERLAP;
+    if (!len) return T3DES_CU_OK;
+    const std::uint64_t nblocks = len / 8;
+    // Contiguous shards [g*N/G, (g+1)*N/G) rounded down to whole tiles.
+    std::vector<std::uint64_t> cut(ndev + 1);
+    for (int g = 0; g <= ndev; ++g) {
+        std::uint64_t b = nblocks * std::uint64_t(g) / std::uint64_t(ndev);
+        if (g < ndev) b -= b % T3_TILE_BLOCKS;
+        cut[g] = g == ndev ? nblocks : b;
+    }
+    std::vector<int> rcs(ndev, T3DES_CU_OK);
+    std::vector<std::thread> workers;
+    for (int g = 0; g < ndev; ++g) {
+        workers.emplace_back([&, g] {
+            const std::uint64_t b0 = cut[g], b1 = cut[g + 1];
+            if (b1 <= b0) return;
+            t3des_cu_ctx* c = nullptr;
+            int rc = t3des_cu_create(devices[g], &c);
+            if (!rc) rc = t3des_cu_set_schedule(c, sub48);
+            if (!rc) rc = t3des_cu_ecb_host(c, dir, in + 8 * b0, out + 8 * b0, 8 * (b1 - b0));
+            if (c) t3des_cu_destroy(c);
+            rcs[g] = rc;
+        });
+    }
+    for (auto& w : workers) w.join();
+    for (int rc : rcs)
+        if (rc) return rc;
+    return T3DES_CU_OK;
+}
+
+int t3des_cu_host_alloc(std::size_t bytes, void** out) {
+    if (!out) return T3DES_CU_ERR_ARG;
+    *out = nullptr;
+    T3_CK(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable));
+    return T3DES_CU_OK;
+}
+
+int t3des_cu_host_free(void* p) {
+    if (p) T3_CK(cudaFreeHost(p));
+    return T3DES_CU_OK;
+}
+
+int t3des_cu_fill_splitmix(t3des_cu_ctx* c, void* dptr, std::uint64_t first_block, std::size_t nblocks,
+                           std::uint64_t seed, void* stream) {
+    if (!c || (nblocks && !dptr)) return T3DES_CU_ERR_ARG;
+    if (!nblocks) return T3DES_CU_OK;
+    DeviceScope scope(c->device);
+    const unsigned grid = unsigned(std::min<std::uint64_t>((nblocks + 255) / 256, std::uint64_t(c->sms) * 8));
+    t3_fill_splitmix_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<uint2*>(dptr), first_block, nblocks, seed);
+    T3_CK(cudaGetLastError());
+    return T3DES_CU_OK;
+}
+
+int t3des_cu_checksum(t3des_cu_ctx* c, const void* dptr, std::uint64_t first_block, std::size_t nblocks,
+                      std::uint64_t* out) {
+    if (!c || !out || (nblocks && !dptr)) return T3DES_CU_ERR_ARG;
+    DeviceScope scope(c->device);
+    cudaStream_t s = c->st[0];
+    unsigned long long h = 0;
+    T3_CK(cudaMemsetAsync(c->d_acc, 0, sizeof h, s));
+    if (nblocks) {
+        const unsigned grid =
+            unsigned(std::min<std::uint64_t>((nblocks + 255) / 256, std::uint64_t(c->sms) * 8));
+        t3_checksum_kernel<<<grid, 256, 0, s>>>(static_cast<const unsigned long long*>(dptr), first_block,
+                                                nblocks, c->d_acc);
+        T3_CK(cudaGetLastError());
+    }
+    T3_CK(cudaMemcpyAsync(&h, c->d_acc, sizeof h, cudaMemcpyDeviceToHost, s));
+    T3_CK(cudaStreamSynchronize(s));
+    *out = h;
+    return T3DES_CU_OK;
+}
+
+int t3des_cu_launch_count(t3des_cu_ctx* c, std::uint64_t* out) {
+    if (!c || !out) return T3DES_CU_ERR_ARG;
+    *out = c->launches;
+    return T3DES_CU_OK;
+}
+
+}  // extern "C"

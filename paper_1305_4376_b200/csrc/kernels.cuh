@@ -1,0 +1,177 @@
+// sm_100a kernels of the B200 3DES-ECB engine.
+//
+//   t3_bs_kernel  bitsliced 3DES (primary): one warp owns a tile of 1024
+//                 blocks (8 KiB), each thread 32 blocks held as 64 slice
+//                 words; loads/stores are coalesced 128-bit (or 64-bit when
+//                 the buffers are only 8-byte aligned), the rounds are pure
+//                 lop3 on the integer pipe with key/whitening constants read
+//                 from constant bank 0 (__grid_constant__ table, LDCU).
+//   t3_sp_kernel  SP-table variant (measured alternative): one block per
+//                 thread per step, the 8 fused S/P tables replicated per lane
+//                 in shared memory (64 KiB, bank = lane: conflict-free).
+//   helpers       splitmix payload generator, order-sensitive checksum.
+//
+// Replaces the reference's Threaded backend inner loop
+// (/root/reference/proj/src/dispatch.cpp:60-86 -> run_blocks_fast :47-56
+// -> tdes_{en,de}crypt_block_fast, tdes.cpp:177-185).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "t3des_core.cuh"
+
+#define T3_BS_THREADS 128
+#define T3_BS_MIN_CTAS 4
+#define T3_SP_THREADS 256
+#define T3_TILE_BLOCKS 1024  // blocks per warp tile (32 lanes x 32 blocks)
+
+struct T3SpKeyParam {
+    uint32_t k[48][8];
+};
+
+// ---- bitsliced kernel --------------------------------------------------
+// VEC = 4: lane t of the warp loads blocks (64j + 2t, 64j + 2t + 1), j < 16,
+//          with one LDG.128 per j (512 contiguous bytes per instruction).
+// VEC = 2: lane t loads block 32k + t, k < 32, with LDG.64.
+// TAIL:    the final partial tile; missing blocks read as zero and are not
+//          stored (only VEC = 2).
+template <int VEC, bool TAIL>
+__global__ void __launch_bounds__(T3_BS_THREADS, T3_BS_MIN_CTAS)
+t3_bs_kernel(const uint8_t* in, uint8_t* out, uint64_t first_tile, uint64_t ntiles,
+             uint64_t nblocks, const __grid_constant__ T3BsTable tab) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t tile = first_tile + warp; tile < first_tile + ntiles; tile += nwarps) {
+        const uint64_t base = tile * T3_TILE_BLOCKS;
+        uint32_t lo[32], hi[32];
+        if (VEC == 4) {
+            const uint4* src = reinterpret_cast<const uint4*>(in + base * 8) + lane;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const uint4 v = __ldcs(src + 32 * j);
+                lo[2 * j] = v.x;
+                hi[2 * j] = v.y;
+                lo[2 * j + 1] = v.z;
+                hi[2 * j + 1] = v.w;
+            }
+        } else {
+            const uint2* src = reinterpret_cast<const uint2*>(in + base * 8) + lane;
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+                uint2 v = make_uint2(0u, 0u);
+                if (!TAIL || base + 32 * k + lane < nblocks) v = __ldcs(src + 32 * k);
+                lo[k] = v.x;
+                hi[k] = v.y;
+            }
+        }
+        t3_tile32(lo, hi, tab.w);
+        if (VEC == 4) {
+            uint4* dst = reinterpret_cast<uint4*>(out + base * 8) + lane;
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                __stcs(dst + 32 * j, make_uint4(lo[2 * j], hi[2 * j], lo[2 * j + 1], hi[2 * j + 1]));
+        } else {
+            uint2* dst = reinterpret_cast<uint2*>(out + base * 8) + lane;
+#pragma unroll
+            for (int k = 0; k < 32; ++k)
+                if (!TAIL || base + 32 * k + lane < nblocks) __stcs(dst + 32 * k, make_uint2(lo[k], hi[k]));
+        }
+    }
+}
+
+// ---- SP-table kernel ---------------------------------------------------
+__device__ __forceinline__ void t3_dswap(uint32_t& a, uint32_t& b, int s, uint32_t m) {
+    const uint32_t w = ((a >> s) ^ b) & m;
+    b ^= w;
+    a ^= w << s;
+}
+
+// Shared-memory table layout: word (i * 64 + six) * 32 + lane, i.e. byte
+// offset i*8192 + six*128 + lane*4.  Keys arrive pre-shifted to bits 7..12.
+__device__ __forceinline__ uint32_t t3_sp_f(uint32_t r, const uint32_t* k, const char* smem_lane) {
+    uint32_t f = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        // E window of S-box i rotated so its 6 bits sit at bits 7..12.
+        const uint32_t y = __funnelshift_r(r, r, (20 - 4 * i) & 31);
+        const uint32_t off = (y ^ k[i]) & 0x1F80u;
+        f |= *reinterpret_cast<const uint32_t*>(smem_lane + i * 8192 + off);
+    }
+    return f;
+}
+
+__global__ void __launch_bounds__(T3_SP_THREADS)
+t3_sp_kernel(const uint2* in, uint2* out, uint64_t nblocks, const uint32_t* __restrict__ sp_global,
+             const __grid_constant__ T3SpKeyParam kp) {
+    extern __shared__ uint32_t t3_sp_smem[];
+    for (int w = threadIdx.x; w < 8 * 64 * 32; w += blockDim.x) t3_sp_smem[w] = sp_global[w >> 5];
+    __syncthreads();
+    const char* smem_lane = reinterpret_cast<const char*>(t3_sp_smem) + (threadIdx.x & 31) * 4;
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t b = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < nblocks; b += stride) {
+        const uint2 v = __ldcs(in + b);
+        uint32_t x = __byte_perm(v.x, 0, 0x0123);  // big-endian high word
+        uint32_t y = __byte_perm(v.y, 0, 0x0123);
+        // IP as five delta swaps (verified against the FIPS table in tests).
+        t3_dswap(x, y, 4, 0x0F0F0F0Fu);
+        t3_dswap(x, y, 16, 0x0000FFFFu);
+        t3_dswap(y, x, 2, 0x33333333u);
+        t3_dswap(y, x, 8, 0x00FF00FFu);
+        t3_dswap(x, y, 1, 0x55555555u);
+#pragma unroll 1
+        for (int t = 0; t < 16; t += 2) {
+            x ^= t3_sp_f(y, kp.k[t], smem_lane);
+            y ^= t3_sp_f(x, kp.k[t + 1], smem_lane);
+        }
+#pragma unroll 1
+        for (int t = 16; t < 32; t += 2) {
+            y ^= t3_sp_f(x, kp.k[t], smem_lane);
+            x ^= t3_sp_f(y, kp.k[t + 1], smem_lane);
+        }
+#pragma unroll 1
+        for (int t = 32; t < 48; t += 2) {
+            x ^= t3_sp_f(y, kp.k[t], smem_lane);
+            y ^= t3_sp_f(x, kp.k[t + 1], smem_lane);
+        }
+        // preoutput = y || x, then FP = the IP swaps in reverse order.
+        uint32_t hi = y, lo = x;
+        t3_dswap(hi, lo, 1, 0x55555555u);
+        t3_dswap(lo, hi, 8, 0x00FF00FFu);
+        t3_dswap(lo, hi, 2, 0x33333333u);
+        t3_dswap(hi, lo, 16, 0x0000FFFFu);
+        t3_dswap(hi, lo, 4, 0x0F0F0F0Fu);
+        __stcs(out + b, make_uint2(__byte_perm(hi, 0, 0x0123), __byte_perm(lo, 0, 0x0123)));
+    }
+}
+
+// ---- helpers -----------------------------------------------------------
+__device__ __forceinline__ uint64_t t3_splitmix(uint64_t seed, uint64_t i) {
+    uint64_t z = (seed ^ i) + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+// Block i (global index first_block + i) = splitmix64(seed ^ index),
+// serialised big-endian (same as oracle_splitmix_payload).
+__global__ void t3_fill_splitmix_kernel(uint2* out, uint64_t first_block, uint64_t n, uint64_t seed) {
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint64_t v = t3_splitmix(seed, first_block + i);
+        out[i] = make_uint2(__byte_perm(uint32_t(v >> 32), 0, 0x0123), __byte_perm(uint32_t(v), 0, 0x0123));
+    }
+}
+
+// Order-sensitive, shard-additive checksum: sum_i splitmix(word_i ^ gidx_i)
+// mod 2^64 where word_i is the little-endian 64-bit load of block i.
+__global__ void t3_checksum_kernel(const unsigned long long* in, uint64_t first_block, uint64_t n,
+                                   unsigned long long* acc) {
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    unsigned long long s = 0;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        s += t3_splitmix(in[i] ^ (first_block + i), 0x3DE5C0DEull);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(acc, s);
+}

@@ -1,0 +1,48 @@
+// Host-side keying for the B200 3DES engine: hex-key parsing, the DES key
+// schedule, the 48-key execution sequence and its expansion into the
+// constant tables the kernels read.  Pure host C++ (no CUDA calls).
+//
+// Reference interfaces restated (semantics, not code):
+//   parse_hex_key   /root/reference/proj/src/tdes.cpp:32-59
+//   key_schedule    /root/reference/proj/src/des.cpp:135-149
+//   triple_schedule /root/reference/proj/src/tdes.cpp:84-87 (pass-major)
+//   key order of tdes_{en,de}crypt_block_fast, tdes.cpp:177-185
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+#include "t3des_core.cuh"
+
+namespace t3b {
+
+// Returns 1/2/3 (keying option) or a negative value: -1 bad length,
+// -2 bad hex character.  Keys are written k1, k2, k3 (k3=k1 for Option 2,
+// all equal for Option 3).
+int parse_hex_key(const char* hex, std::size_t len, std::uint64_t keys[3]);
+
+// 16 round keys of 48 bits (FIPS bit 1 of the subkey at machine bit 47).
+void des_key_schedule(std::uint64_t key, std::uint64_t ks[16]);
+
+// 48 subkeys, pass-major: k1's 16, then k2's, then k3's.
+void triple_schedule(const std::uint64_t keys[3], std::uint64_t sub48[48]);
+
+// The 48 round keys in execution order: encrypt = k1 fwd, k2 rev, k3 fwd;
+// decrypt = the exact reverse sequence.
+void key_sequence(const std::uint64_t sub48[48], bool decrypt, std::uint64_t seq[48]);
+
+// Whitening/key-constant table of the bitsliced kernel for one execution
+// sequence (layout: T3_TAB_* in t3des_core.cuh).
+void build_bitslice_table(const std::uint64_t seq[48], T3BsTable& tab);
+
+// Per-round 6-bit key chunks for the SP-table kernel: k6[r][i] is the key
+// input of S-box i in round r, shifted to bits 7..12 (pre-scaled as a byte
+// offset of a 128-byte row).
+struct SpKeys {
+    std::uint32_t k[48][8];
+};
+void build_sp_keys(const std::uint64_t seq[48], SpKeys& out);
+
+// The eight S-box/P fused tables (2 KiB): sp[i][six] = P(S_i(six) placed).
+void build_sp_tables(std::uint32_t sp[8][64]);
+
+}  // namespace t3b

@@ -1,0 +1,140 @@
+// C++ host API (include/t3des_b200/t3des.hpp) over the C ABI.
+#include "t3des_b200/t3des.hpp"
+
+#include <cstring>
+#include <map>
+#include <memory>
+
+#include "schedule.hpp"
+#include "t3des_cu.h"
+
+namespace t3des {
+namespace {
+
+[[noreturn]] void raise(int rc) {
+    if (rc == T3DES_CU_ERR_LENGTH || rc == T3DES_CU_ERR_OVERLAP)
+        throw InputLengthError(t3des_cu_strerror(rc));
+    if (rc == T3DES_CU_ERR_KEY) throw KeyFormatError(t3des_cu_strerror(rc));
+    throw CudaError(std::string("t3des_cu: ") + t3des_cu_strerror(rc), rc);
+}
+
+struct CtxDeleter {
+    void operator()(t3des_cu_ctx* c) const { t3des_cu_destroy(c); }
+};
+
+// One context per device per submitting thread (SPEC.md:233 threading).
+t3des_cu_ctx* context_for(int device) {
+    thread_local std::map<int, std::unique_ptr<t3des_cu_ctx, CtxDeleter>> cache;
+    auto it = cache.find(device);
+    if (it != cache.end()) return it->second.get();
+    t3des_cu_ctx* c = nullptr;
+    const int rc = t3des_cu_create(device, &c);
+    if (rc) raise(rc);
+    cache.emplace(device, std::unique_ptr<t3des_cu_ctx, CtxDeleter>(c));
+    return c;
+}
+
+void flatten(const TripleSchedule& ts, std::uint64_t sub48[48]) {
+    std::memcpy(sub48, ts.pass1.data(), 16 * 8);
+    std::memcpy(sub48 + 16, ts.pass2.data(), 16 * 8);
+    std::memcpy(sub48 + 32, ts.pass3.data(), 16 * 8);
+}
+
+// Reference run_batch (dispatch.cpp:88-109) with the CUDA branch taken
+// before the span loop: one C-ABI call per batch.
+void run_batch(std::span<const std::uint8_t> in, std::span<std::uint8_t> out, const TripleSchedule& ts,
+               const DispatchConfig& cfg, int dir) {
+    if (in.size() % 8 != 0)
+        throw InputLengthError("batch length " + std::to_string(in.size()) + " is not a multiple of 8 bytes");
+    if (out.size() != in.size()) throw InputLengthError("output buffer size mismatch");
+    const auto* ib = in.data();
+    if (out.data() != ib && out.data() < ib + in.size() && out.data() + out.size() > ib)
+        throw InputLengthError("partially overlapping buffers");
+    switch (cfg.backend) {
+        case Backend::NoOpCopy:
+            if (out.data() != ib && !in.empty()) std::memmove(out.data(), ib, in.size());
+            return;
+        case Backend::ScalarReference:
+        case Backend::Threaded:
+            throw std::invalid_argument(
+                "t3des B200 engine: only Backend::Cuda (and NoOpCopy) are provided; the CPU backends "
+                "live in the reference library");
+        case Backend::Cuda:
+            break;
+    }
+    if (in.empty()) return;
+    std::uint64_t sub48[48];
+    flatten(ts, sub48);
+    const unsigned ngpu = cfg.workers == 0 ? 1u : cfg.workers;
+    int rc;
+    if (ngpu > 1) {
+        std::vector<int> devs(ngpu);
+        for (unsigned g = 0; g < ngpu; ++g) devs[g] = cfg.device + static_cast<int>(g);
+        rc = t3des_cu_ecb_multi(devs.data(), static_cast<int>(ngpu), sub48, dir, ib, out.data(), in.size());
+    } else {
+        t3des_cu_ctx* c = context_for(cfg.device);
+        rc = t3des_cu_set_schedule(c, sub48);
+        if (!rc) rc = t3des_cu_set_variant(c, cfg.variant);
+        if (!rc)
+            rc = cfg.gpu_chunked ? t3des_cu_set_launch(c, cfg.chunk_blocks, static_cast<int>(cfg.work_group))
+                                 : t3des_cu_set_launch(c, 0, 0);
+        if (!rc) rc = t3des_cu_ecb_host(c, dir, ib, out.data(), in.size());
+    }
+    if (rc) raise(rc);
+}
+
+}  // namespace
+
+TripleKey parse_hex_key(std::string_view hex) {
+    std::uint64_t k[3];
+    const int opt = t3b::parse_hex_key(hex.data(), hex.size(), k);
+    if (opt == -1)
+        throw KeyFormatError("key must be 16, 32 or 48 hex characters, got " + std::to_string(hex.size()));
+    if (opt < 0) throw KeyFormatError("invalid hex character in key");
+    TripleKey key;
+    key.k1.raw = k[0];
+    key.k2.raw = k[1];
+    key.k3.raw = k[2];
+    key.option = opt == 1 ? KeyingOption::Option1 : (opt == 2 ? KeyingOption::Option2 : KeyingOption::Option3);
+    return key;
+}
+
+RoundKeySet key_schedule(DesKey key) {
+    RoundKeySet ks{};
+    t3b::des_key_schedule(key.raw, ks.data());
+    return ks;
+}
+
+TripleSchedule triple_schedule(const TripleKey& key) {
+    return TripleSchedule{key_schedule(key.k1), key_schedule(key.k2), key_schedule(key.k3)};
+}
+
+Block load_block(std::span<const std::uint8_t, 8> bytes) {
+    Block b = 0;
+    for (int i = 0; i < 8; ++i) b |= static_cast<Block>(bytes[i]) << (56 - 8 * i);
+    return b;
+}
+
+void store_block(Block b, std::span<std::uint8_t, 8> out) {
+    for (int i = 0; i < 8; ++i) out[i] = static_cast<std::uint8_t>(b >> (56 - 8 * i));
+}
+
+std::vector<ChunkSpan> plan_dispatch(std::size_t total_blocks, const DispatchConfig& cfg) {
+    std::vector<ChunkSpan> spans;
+    const std::size_t step = cfg.chunk_blocks ? cfg.chunk_blocks : (total_blocks ? total_blocks : 1);
+    for (std::size_t off = 0; off < total_blocks; off += step)
+        spans.push_back(ChunkSpan{off, step < total_blocks - off ? step : total_blocks - off});
+    return spans;
+}
+
+void encrypt_batch(std::span<const std::uint8_t> in, std::span<std::uint8_t> out, const TripleSchedule& ts,
+                   const DispatchConfig& cfg) {
+    run_batch(in, out, ts, cfg, T3DES_CU_ENCRYPT);
+}
+
+void decrypt_batch(std::span<const std::uint8_t> in, std::span<std::uint8_t> out, const TripleSchedule& ts,
+                   const DispatchConfig& cfg) {
+    run_batch(in, out, ts, cfg, T3DES_CU_DECRYPT);
+}
+
+}  // namespace t3des

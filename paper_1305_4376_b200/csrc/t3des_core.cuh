@@ -1,0 +1,161 @@
+// Bitsliced 3DES core for sm_100a: 32x32 slice transposes, the 48-round
+// cipher over 64 slice words, and the whitening-table layout.
+//
+// Portable between device code and a host test build (tests/native): the
+// only device-specific pieces are lop3 and prmt, which fall back to plain C
+// when __CUDA_ARCH__ is not defined.  The host build exists so the test
+// suite can check the generated round code on a CPU; the product path is
+// the CUDA kernel in bitslice_kernel.cuh and never runs this on the host.
+//
+// Reference path replaced: fused_tdes / run_pass / round_f
+// (/root/reference/proj/src/tdes.cpp:132-173) and the per-block loop
+// run_blocks_fast (dispatch.cpp:47-56).
+#pragma once
+#include <stdint.h>
+
+#ifdef __CUDACC__
+#define T3_FI __host__ __device__ __forceinline__
+#else
+#define T3_FI inline
+#endif
+
+template <unsigned LUT>
+T3_FI uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
+#ifdef __CUDA_ARCH__
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(d) : "r"(a), "r"(b), "r"(c), "n"(LUT));
+    return d;
+#else
+    uint32_t r = 0;
+#pragma unroll
+    for (int m = 0; m < 8; ++m)
+        if ((LUT >> m) & 1u)
+            r |= ((m & 4) ? a : ~a) & ((m & 2) ? b : ~b) & ((m & 1) ? c : ~c);
+    return r;
+#endif
+}
+
+template <unsigned SEL>
+T3_FI uint32_t prmt(uint32_t a, uint32_t b) {
+#ifdef __CUDA_ARCH__
+    return __byte_perm(a, b, SEL);
+#else
+    const uint64_t v = ((uint64_t)b << 32) | a;
+    uint32_t r = 0;
+    for (int i = 0; i < 4; ++i) r |= (uint32_t)((v >> (8 * ((SEL >> (4 * i)) & 7))) & 0xFF) << (8 * i);
+    return r;
+#endif
+}
+
+#include "generated/bitslice_rounds.cuh"
+
+// ---- whitening/key table (built on the host, schedule.cpp) --------------
+// Word offsets inside the 2496-word table that travels as the kernel's
+// __grid_constant__ parameter (constant bank 0, read through LDCU).
+enum : int {
+    T3_TAB_PRE = 0,            // 64: initial whitening, half A then half B
+    T3_TAB_ROUND = 64,         // 48 rounds x 48 words (32 C + 16 D)
+    T3_TAB_RW1 = 64 + 48 * 48, // 32: re-whitening of A between pass 1 and 2
+    T3_TAB_RW2 = T3_TAB_RW1 + 32,  // 32: re-whitening of B between pass 2 and 3
+    T3_TAB_POST = T3_TAB_RW2 + 32, // 64: final un-whitening, A then B
+    T3_TAB_WORDS = T3_TAB_POST + 64,
+};
+
+struct T3BsTable {
+    uint32_t w[T3_TAB_WORDS];
+};
+
+// In-register transpose of a 32x32 bit matrix: afterwards x[k] bit m is the
+// old x[m] bit k.  Stages 16 and 8 are byte moves (PRMT); stages 4, 2, 1
+// are mask-select swaps (two shifts + two lop3 per pair).
+T3_FI void t3_transpose32(uint32_t (&x)[32]) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        const uint32_t a = x[r], b = x[r + 16];
+        x[r] = prmt<0x5410>(a, b);
+        x[r + 16] = prmt<0x7632>(a, b);
+    }
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+        if (r & 8) continue;
+        const uint32_t a = x[r], b = x[r + 8];
+        x[r] = prmt<0x6240>(a, b);
+        x[r + 8] = prmt<0x7351>(a, b);
+    }
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+        if (r & 4) continue;
+        const uint32_t a = x[r], b = x[r + 4];
+        x[r] = lop3<0xE4>(a, b << 4, 0x0F0F0F0Fu);  // 0xE4: c ? a : b
+        x[r + 4] = lop3<0xE4>(a >> 4, b, 0x0F0F0F0Fu);
+    }
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+        if (r & 2) continue;
+        const uint32_t a = x[r], b = x[r + 2];
+        x[r] = lop3<0xE4>(a, b << 2, 0x33333333u);
+        x[r + 2] = lop3<0xE4>(a >> 2, b, 0x33333333u);
+    }
+#pragma unroll
+    for (int r = 0; r < 32; r += 2) {
+        const uint32_t a = x[r], b = x[r + 1];
+        x[r] = lop3<0xE4>(a, b << 1, 0x55555555u);
+        x[r + 1] = lop3<0xE4>(a >> 1, b, 0x55555555u);
+    }
+}
+
+template <class KP>
+T3_FI void t3_xor_table(uint32_t (&h)[32], const KP k) {
+#pragma unroll
+    for (int q = 0; q < 32; ++q) h[q] ^= k[q];
+}
+
+// All 48 rounds (3 passes of 16) on halves A (initial L) and B (initial R).
+// The pass-final half swaps of the reference (tdes.cpp:151-159) are role
+// renamings: pass 2 runs with the roles of A and B exchanged.
+template <class KP>
+T3_FI void t3_cipher(uint32_t (&A)[32], uint32_t (&B)[32], const KP w) {
+    t3_xor_table(A, w + T3_TAB_PRE);
+    t3_xor_table(B, w + T3_TAB_PRE + 32);
+#pragma unroll 1
+    for (int it = 0; it < 8; ++it) {
+        t3_round(A, B, w + T3_TAB_ROUND + (2 * it) * 48);
+        t3_round(B, A, w + T3_TAB_ROUND + (2 * it + 1) * 48);
+    }
+    t3_xor_table(A, w + T3_TAB_RW1);
+#pragma unroll 1
+    for (int it = 0; it < 8; ++it) {
+        t3_round(B, A, w + T3_TAB_ROUND + (16 + 2 * it) * 48);
+        t3_round(A, B, w + T3_TAB_ROUND + (17 + 2 * it) * 48);
+    }
+    t3_xor_table(B, w + T3_TAB_RW2);
+#pragma unroll 1
+    for (int it = 0; it < 8; ++it) {
+        t3_round(A, B, w + T3_TAB_ROUND + (32 + 2 * it) * 48);
+        t3_round(B, A, w + T3_TAB_ROUND + (33 + 2 * it) * 48);
+    }
+    t3_xor_table(A, w + T3_TAB_POST);
+    t3_xor_table(B, w + T3_TAB_POST + 32);
+}
+
+// One thread's 32 blocks: lo[m]/hi[m] are the little-endian words holding
+// bytes 0..3 / 4..7 of block m.  Transforms in place.
+template <class KP>
+T3_FI void t3_tile32(uint32_t (&lo)[32], uint32_t (&hi)[32], const KP w) {
+    t3_transpose32(lo);
+    t3_transpose32(hi);
+    uint32_t A[32] = T3_GATHER_A(lo, hi);
+    uint32_t B[32] = T3_GATHER_B(lo, hi);
+    t3_cipher(A, B, w);
+    {
+        uint32_t olo[32] = T3_SCATTER_LO(A, B);
+        uint32_t ohi[32] = T3_SCATTER_HI(A, B);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+            lo[k] = olo[k];
+            hi[k] = ohi[k];
+        }
+    }
+    t3_transpose32(lo);
+    t3_transpose32(hi);
+}

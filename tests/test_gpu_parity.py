@@ -1,0 +1,253 @@
+"""GPU parity: the sm_100a kernels through the C ABI against the CPU oracle
+(bit-exact — integer work), the reference's golden vectors, and at
+BASELINE.json's full sizes through size-independent properties
+(round trip, variant agreement, checksum invariance, sampled oracle blocks).
+"""
+import ctypes
+import hashlib
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+import paper_1305_4376_b200 as t3  # noqa: E402
+from paper_1305_4376_b200 import _native as N  # noqa: E402
+from tests.oracle_util import ROOT, checksum, sub48_from_hex_list  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+BENCH_KEY = "133457799BBCDFF10E329232EA6D0D737CA110454A1A6E57"
+KEYS = [BENCH_KEY, "0123456789ABCDEF23456789ABCDEF01", "0123456789ABCDEF"]
+VARIANTS = [N.VARIANT_BITSLICE, N.VARIANT_SPTABLE]
+
+
+def dev(a: np.ndarray, pad: int = 0):
+    """uint8 CUDA tensor holding `a`, optionally starting `pad` bytes into a
+    256-aligned allocation (pad=8 exercises the 64-bit load path)."""
+    buf = torch.empty(a.nbytes + pad + 16, dtype=torch.uint8, device="cuda")
+    t = buf[pad: pad + a.nbytes]
+    if a.nbytes:
+        t.copy_(torch.from_numpy(a))
+    return t
+
+
+def host(t) -> np.ndarray:
+    return t.cpu().numpy()
+
+
+@pytest.fixture(scope="module")
+def eng(engine_lib):
+    e = t3.Engine(0)
+    yield e
+    e.close()
+
+
+def run(e, ts, x: np.ndarray, d: int, variant=N.VARIANT_BITSLICE, pad=0, inplace=False, chunk=0, wg=0):
+    e.set_schedule(ts)
+    e.set_variant(variant)
+    e.set_launch(chunk, wg)
+    src = dev(x, pad)
+    dst = src if inplace else dev(np.zeros_like(x), pad)
+    e.ecb_device(d, src.data_ptr(), dst.data_ptr(), x.nbytes, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    return host(dst)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_kats_on_device(eng, golden, variant):
+    for kat in golden["kats"]["tdes"]:
+        ts = t3.triple_schedule(t3.parse_hex_key(kat["key"]))
+        pt = np.frombuffer(bytes.fromhex(kat["plaintext"]), dtype=np.uint8).copy()
+        ct = run(eng, ts, pt, 0, variant)
+        assert ct.tobytes().hex().upper() == kat["ciphertext"]
+        assert run(eng, ts, ct, 1, variant).tobytes() == pt.tobytes()
+    for kat in golden["kats"]["des"]:  # option 3 == single DES
+        ts = t3.triple_schedule(t3.parse_hex_key(kat["key"]))
+        pt = np.frombuffer(bytes.fromhex(kat["plaintext"]), dtype=np.uint8).copy()
+        assert run(eng, ts, pt, 0, variant).tobytes().hex().upper() == kat["ciphertext"]
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_golden_batches_on_device(eng, oracle, golden, variant):
+    for rec in golden["batches"]:
+        ts = t3.triple_schedule(t3.parse_hex_key(golden["schedules"][rec["key"]]["key"]))
+        x = oracle.payload(8 * rec["nblocks"], rec["payload_seed"])
+        y = run(eng, ts, x, rec["decrypt"], variant)
+        assert hashlib.sha256(y.tobytes()).hexdigest() == rec["sha256"], rec
+
+
+@pytest.mark.parametrize("keyhex", KEYS)
+@pytest.mark.parametrize("n", [1, 31, 32, 33, 1023, 1024, 1025, 2047, 8195, 131071, 131072, 1000003])
+def test_edge_counts_vs_oracle(eng, oracle, keyhex, n):
+    ts = t3.triple_schedule(t3.parse_hex_key(keyhex))
+    s = oracle.schedule_hex(keyhex)
+    x = np.random.default_rng(n).integers(0, 256, 8 * n, dtype=np.uint8)
+    for d in (0, 1):
+        want = oracle.ecb(x, s, d)
+        for variant in VARIANTS:
+            assert np.array_equal(run(eng, ts, x, d, variant), want), (n, d, variant)
+        assert np.array_equal(run(eng, ts, x, d, pad=8), want), "64-bit path"
+        assert np.array_equal(run(eng, ts, x, d, inplace=True), want), "in place"
+
+
+def test_chunk_and_work_group_invariance(eng, oracle):
+    # test_dispatch.cpp:111-129: ciphertext invariant over chunk x wg, odd tail
+    ts = t3.triple_schedule(t3.parse_hex_key(KEYS[0]))
+    x = oracle.payload(8 * 8195)
+    want = oracle.ecb(x, oracle.schedule_hex(KEYS[0]), 0)
+    for chunk in (1, 7, 1024, 131072):
+        for wg in (32, 64, 128):
+            assert np.array_equal(run(eng, ts, x, 0, chunk=chunk, wg=wg), want), (chunk, wg)
+            assert np.array_equal(run(eng, ts, x, 0, N.VARIANT_SPTABLE, chunk=chunk, wg=wg), want)
+
+
+def test_device_errors(eng):
+    ts = t3.triple_schedule(t3.parse_hex_key(KEYS[0]))
+    eng.set_schedule(ts)
+    a = torch.zeros(64, dtype=torch.uint8, device="cuda")
+    with pytest.raises(t3.InputLengthError):
+        eng.ecb_device(0, a.data_ptr(), a.data_ptr(), 60)
+    with pytest.raises(t3.InputLengthError):
+        eng.ecb_device(0, a.data_ptr(), a.data_ptr() + 8, 56)
+    fresh = t3.Engine(0)
+    with pytest.raises(t3.CudaError):
+        fresh.ecb_device(0, a.data_ptr(), a.data_ptr(), 64)  # no schedule installed
+    fresh.close()
+
+
+def test_host_path_pipeline(eng, oracle):
+    """t3des_cu_ecb_host: >64 MiB to cross several pipeline chunks, pageable
+    and pinned buffers, in place."""
+    ts = t3.triple_schedule(t3.parse_hex_key(KEYS[0]))
+    s = oracle.schedule_hex(KEYS[0])
+    n = (200 << 20) // 8 + 5
+    x = oracle.splitmix(0, n, 99)
+    eng.set_schedule(ts)
+    eng.set_variant(N.VARIANT_BITSLICE)
+    eng.set_launch(0, 0)
+    y = np.empty_like(x)
+    eng.ecb_host(0, x.ctypes.data, y.ctypes.data, x.nbytes)
+    idx = np.random.default_rng(0).integers(0, n, 4000)
+    idx = np.unique(np.concatenate([idx, [0, n - 1, (64 << 20) // 8 - 1, (64 << 20) // 8]]))
+    for i in idx[:: max(1, len(idx) // 500)]:
+        assert oracle.ecb(x[8 * i: 8 * i + 8], s, 0).tobytes() == y[8 * i: 8 * i + 8].tobytes(), i
+    pinned = torch.empty(x.nbytes, dtype=torch.uint8).pin_memory()
+    pinned.numpy()[:] = y
+    eng.ecb_host(1, pinned.data_ptr(), pinned.data_ptr(), x.nbytes)  # in place
+    assert np.array_equal(pinned.numpy(), x)
+
+
+def test_python_api_host_and_device(oracle):
+    ts = t3.triple_schedule(t3.parse_hex_key(KEYS[1]))
+    s = oracle.schedule_hex(KEYS[1])
+    x = oracle.payload(8 * 5000)
+    out = bytearray(x.nbytes)
+    t3.encrypt_batch(x.tobytes(), out, ts)
+    assert bytes(out) == oracle.ecb(x, s, 0).tobytes()
+    d = torch.from_numpy(np.frombuffer(bytes(out), dtype=np.uint8).copy()).cuda()
+    t3.decrypt_batch(d, d, ts)  # in place on the current stream
+    assert np.array_equal(d.cpu().numpy(), x)
+
+
+def test_multi_device_api_shards(oracle):
+    """t3des_cu_ecb_multi block-range sharding; on a 1-GPU box the shards go
+    to two contexts on device 0 (independent kernels, no cross-waiting)."""
+    ngpu = torch.cuda.device_count()
+    devs = list(range(ngpu)) if ngpu > 1 else [0, 0]
+    s = oracle.schedule_hex(KEYS[0])
+    x = oracle.payload(8 * (3 * 1024 * 7 + 11))
+    y = np.empty_like(x)
+    arr = (ctypes.c_int * len(devs))(*devs)
+    rc = N.lib().t3des_cu_ecb_multi(arr, len(devs), s, 0, x.ctypes.data, y.ctypes.data, x.nbytes)
+    assert rc == 0
+    assert np.array_equal(y, oracle.ecb(x, s, 0))
+
+
+def test_fill_and_checksum_kernels(eng, oracle):
+    n = 1 << 16
+    t = torch.empty(8 * n, dtype=torch.uint8, device="cuda")
+    eng.fill_splitmix(t.data_ptr(), 12345, n, 77)
+    torch.cuda.synchronize()
+    x = oracle.splitmix(12345, n, 77)
+    assert np.array_equal(t.cpu().numpy(), x)
+    assert eng.checksum(t.data_ptr(), 12345, n) == checksum(x, 12345)
+    # shard-additive
+    half = n // 2
+    a = eng.checksum(t.data_ptr(), 12345, half)
+    b = eng.checksum(t.data_ptr() + 8 * half, 12345 + half, n - half)
+    assert (a + b) % 2**64 == checksum(x, 12345)
+
+
+@pytest.mark.parametrize("gib,direction", [(1, 0), (4, 1)])
+def test_full_size_configs(eng, oracle, gib, direction):
+    """BASELINE configs[1] (1 GiB encrypt, bitsliced vs SP-table) and
+    configs[2] (4 GiB decrypt): variants agree bit-exactly, decrypt inverts
+    encrypt (checksum of the round trip), sampled blocks match the oracle."""
+    ts = t3.triple_schedule(t3.parse_hex_key(BENCH_KEY))
+    s = oracle.schedule_hex(BENCH_KEY)
+    n = (gib << 30) // 8
+    seed = 0x3DE5C0DE
+    buf = torch.empty(8 * n, dtype=torch.uint8, device="cuda")
+    eng.fill_splitmix(buf.data_ptr(), 0, n, seed)
+    cs_plain = eng.checksum(buf.data_ptr(), 0, n)
+    stream = torch.cuda.current_stream().cuda_stream
+    eng.set_schedule(ts)
+    eng.set_launch(0, 0)
+    if direction == 1:  # make ciphertext first
+        eng.set_variant(N.VARIANT_BITSLICE)
+        eng.ecb_device(0, buf.data_ptr(), buf.data_ptr(), 8 * n, stream)
+    out = torch.empty_like(buf)
+    eng.set_variant(N.VARIANT_BITSLICE)
+    eng.ecb_device(direction, buf.data_ptr(), out.data_ptr(), 8 * n, stream)
+    cs_bs = eng.checksum(out.data_ptr(), 0, n)
+    if gib == 1:
+        eng.set_variant(N.VARIANT_SPTABLE)
+        out2 = torch.empty_like(buf)
+        eng.ecb_device(direction, buf.data_ptr(), out2.data_ptr(), 8 * n, stream)
+        assert eng.checksum(out2.data_ptr(), 0, n) == cs_bs
+        assert torch.equal(out2, out)
+        del out2
+    rng = np.random.default_rng(gib)
+    idx = np.unique(np.concatenate([rng.integers(0, n, 2000), [0, 1023, 1024, n - 1]]))
+    src = buf.view(torch.int64)[torch.from_numpy(idx).cuda()].cpu().numpy().view(np.uint8)
+    got = out.view(torch.int64)[torch.from_numpy(idx).cuda()].cpu().numpy().view(np.uint8)
+    assert np.array_equal(got, oracle.ecb(src, s, direction))
+    if direction == 1:
+        assert cs_bs == cs_plain  # decrypt(encrypt(p)) == p
+    else:
+        eng.set_variant(N.VARIANT_BITSLICE)
+        eng.ecb_device(1, out.data_ptr(), out.data_ptr(), 8 * n, stream)
+        assert eng.checksum(out.data_ptr(), 0, n) == cs_plain
+    assert eng.launch_count() > 0
+
+
+def test_cpp_api_on_device(engine_lib, oracle, tmp_path):
+    """The C++ mirror of encrypt_batch/decrypt_batch with Backend::Cuda."""
+    src = tmp_path / "t.cpp"
+    src.write_text(r'''
+#include <cstdio>
+#include <vector>
+#include "t3des_b200/t3des.hpp"
+using namespace t3des;
+int main(int argc, char** argv) {
+    auto ts = triple_schedule(parse_hex_key(argv[1]));
+    std::vector<std::uint8_t> in(8 * 8195), out(in.size()), back(in.size());
+    for (std::size_t i = 0; i < in.size(); ++i) in[i] = static_cast<std::uint8_t>(i * 131 + 7);
+    encrypt_batch(in, out, ts, DispatchConfig{});
+    decrypt_batch(out, back, ts, DispatchConfig{});
+    if (back != in) return 3;
+    std::FILE* f = std::fopen(argv[2], "wb");
+    std::fwrite(out.data(), 1, out.size(), f);
+    std::fclose(f);
+    return 0;
+}
+''')
+    exe = tmp_path / "t"
+    subprocess.check_call(["/usr/bin/g++", "-std=c++20", "-I" + os.path.join(ROOT, "include"), str(src),
+                           N.LIB_PATH, "-Wl,-rpath," + os.path.dirname(N.LIB_PATH), "-o", str(exe)])
+    outp = tmp_path / "ct.bin"
+    subprocess.check_call([str(exe), KEYS[0], str(outp)])
+    x = (np.arange(8 * 8195, dtype=np.uint64) * 131 + 7).astype(np.uint8)
+    assert outp.read_bytes() == oracle.ecb(x, oracle.schedule_hex(KEYS[0]), 0).tobytes()

@@ -1,0 +1,361 @@
+/*
+ * sboxgen — offline search for LOP3 (3-input LUT) circuits of the eight DES
+ * S-boxes, for the bitsliced sm_100a kernel.
+ *
+ * The S-box truth tables are the FIPS 46-3 tables (the same data as
+ * /root/reference/proj/src/des.cpp:43-75); the input indexing follows the
+ * reference lookup: row = ((six>>4)&2)|(six&1), col = (six>>1)&0xF
+ * (des.cpp:91-93, tdes.cpp:116-118).
+ *
+ * Method (a Kwan-style recursive decomposition generalised to LUT3 gates):
+ *   build(T, M): find a gate whose truth table equals T (or ~T: every
+ *   consumer is itself a LUT3 or the Feistel XOR, both of which absorb an
+ *   inversion for free) on the care mask M;
+ *   else a new LUT3 over any three existing gates;
+ *   else two new gates LUT3(LUT3(a,b,c), x, y);
+ *   else split on an S-box input s: build the s=0 half, build the s=1 half
+ *   (relative to the s=0 result: mux / xor / and / or forms), and join with
+ *   one LUT3(s, f0, f1).
+ * Outputs are built one after another in random orders, reusing all gates
+ * built so far; many randomised restarts keep the smallest circuit.
+ * Output: one line per gate, consumed by tools/sboxgen/emit.py.
+ *
+ * Usage: sboxgen <sbox 0..7> <iterations> <seed> [max_gates [out_file]]
+ * (out_file is rewritten each time a smaller circuit is found)
+ */
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef uint64_t tt_t;
+#define MAXG 96
+
+static const uint8_t SBOX[8][64] = {
+    {14, 4, 13, 1, 2, 15, 11, 8, 3, 10, 6, 12, 5, 9, 0, 7,
+     0, 15, 7, 4, 14, 2, 13, 1, 10, 6, 12, 11, 9, 5, 3, 8,
+     4, 1, 14, 8, 13, 6, 2, 11, 15, 12, 9, 7, 3, 10, 5, 0,
+     15, 12, 8, 2, 4, 9, 1, 7, 5, 11, 3, 14, 10, 0, 6, 13},
+    {15, 1, 8, 14, 6, 11, 3, 4, 9, 7, 2, 13, 12, 0, 5, 10,
+     3, 13, 4, 7, 15, 2, 8, 14, 12, 0, 1, 10, 6, 9, 11, 5,
+     0, 14, 7, 11, 10, 4, 13, 1, 5, 8, 12, 6, 9, 3, 2, 15,
+     13, 8, 10, 1, 3, 15, 4, 2, 11, 6, 7, 12, 0, 5, 14, 9},
+    {10, 0, 9, 14, 6, 3, 15, 5, 1, 13, 12, 7, 11, 4, 2, 8,
+     13, 7, 0, 9, 3, 4, 6, 10, 2, 8, 5, 14, 12, 11, 15, 1,
+     13, 6, 4, 9, 8, 15, 3, 0, 11, 1, 2, 12, 5, 10, 14, 7,
+     1, 10, 13, 0, 6, 9, 8, 7, 4, 15, 14, 3, 11, 5, 2, 12},
+    {7, 13, 14, 3, 0, 6, 9, 10, 1, 2, 8, 5, 11, 12, 4, 15,
+     13, 8, 11, 5, 6, 15, 0, 3, 4, 7, 2, 12, 1, 10, 14, 9,
+     10, 6, 9, 0, 12, 11, 7, 13, 15, 1, 3, 14, 5, 2, 8, 4,
+     3, 15, 0, 6, 10, 1, 13, 8, 9, 4, 5, 11, 12, 7, 2, 14},
+    {2, 12, 4, 1, 7, 10, 11, 6, 8, 5, 3, 15, 13, 0, 14, 9,
+     14, 11, 2, 12, 4, 7, 13, 1, 5, 0, 15, 10, 3, 9, 8, 6,
+     4, 2, 1, 11, 10, 13, 7, 8, 15, 9, 12, 5, 6, 3, 0, 14,
+     11, 8, 12, 7, 1, 14, 2, 13, 6, 15, 0, 9, 10, 4, 5, 3},
+    {12, 1, 10, 15, 9, 2, 6, 8, 0, 13, 3, 4, 14, 7, 5, 11,
+     10, 15, 4, 2, 7, 12, 9, 5, 6, 1, 13, 14, 0, 11, 3, 8,
+     9, 14, 15, 5, 2, 8, 12, 3, 7, 0, 4, 10, 1, 13, 11, 6,
+     4, 3, 2, 12, 9, 5, 15, 10, 11, 14, 1, 7, 6, 0, 8, 13},
+    {4, 11, 2, 14, 15, 0, 8, 13, 3, 12, 9, 7, 5, 10, 6, 1,
+     13, 0, 11, 7, 4, 9, 1, 10, 14, 3, 5, 12, 2, 15, 8, 6,
+     1, 4, 11, 13, 12, 3, 7, 14, 10, 15, 6, 8, 0, 5, 9, 2,
+     6, 11, 13, 8, 1, 4, 10, 7, 9, 5, 0, 15, 14, 2, 3, 12},
+    {13, 2, 8, 4, 6, 15, 11, 1, 10, 9, 3, 14, 5, 0, 12, 7,
+     1, 15, 13, 8, 10, 3, 7, 4, 12, 5, 6, 11, 0, 14, 9, 2,
+     7, 11, 4, 1, 9, 12, 14, 2, 0, 6, 10, 13, 15, 3, 5, 8,
+     2, 1, 14, 7, 4, 10, 8, 13, 15, 12, 9, 0, 3, 5, 6, 11}};
+
+typedef struct {
+    int n;
+    tt_t tt[MAXG];
+    int in[MAXG][3];
+    uint8_t lut[MAXG];
+} circ_t;
+
+static int g_budget = 40;  /* max gates (including the 6 inputs) */
+static int g_deep5 = 1;    /* enable the 2-gate search */
+static uint64_t g_rng = 88172645463325252ull;
+
+static uint64_t rnd(void) {
+    g_rng ^= g_rng << 13;
+    g_rng ^= g_rng >> 7;
+    g_rng ^= g_rng << 17;
+    return g_rng;
+}
+
+static tt_t lut_eval(uint8_t lut, tt_t a, tt_t b, tt_t c) {
+    tt_t r = 0;
+    for (int m = 0; m < 8; m++)
+        if ((lut >> m) & 1)
+            r |= ((m & 4) ? a : ~a) & ((m & 2) ? b : ~b) & ((m & 1) ? c : ~c);
+    return r;
+}
+
+/* Is there a LUT with LUT(a,b,c) == T on M?  Unconstrained minterms get 0. */
+static int find_lut3(tt_t a, tt_t b, tt_t c, tt_t T, tt_t M, uint8_t* lut) {
+    uint8_t l = 0;
+    for (int m = 0; m < 8; m++) {
+        tt_t P = M & ((m & 4) ? a : ~a) & ((m & 2) ? b : ~b) & ((m & 1) ? c : ~c);
+        tt_t t = T & P;
+        if (t == 0) continue;
+        if (t != P) return 0;
+        l |= (uint8_t)(1u << m);
+    }
+    *lut = l;
+    return 1;
+}
+
+static int add_gate(circ_t* st, int a, int b, int c, uint8_t lut) {
+    int g = st->n++;
+    st->in[g][0] = a;
+    st->in[g][1] = b;
+    st->in[g][2] = c;
+    st->lut[g] = lut;
+    st->tt[g] = lut_eval(lut, st->tt[a], st->tt[b], st->tt[c]);
+    return g;
+}
+
+/* --- 2-gate search: LUT3(h, x, y), h = LUT3(a, b, c) --------------------- */
+/* Parity union-find over 12 nodes: 0..7 = h(m), 8..11 = pol(q). */
+static int uf_p[12], uf_x[12];
+static int uf_find(int v, int* par) {
+    int x = 0;
+    while (uf_p[v] != v) { x ^= uf_x[v]; v = uf_p[v]; }
+    *par = x;
+    return v;
+}
+static int uf_union(int a, int b, int rel) {
+    int pa, pb;
+    int ra = uf_find(a, &pa), rb = uf_find(b, &pb);
+    if (ra == rb) return ((pa ^ pb) == rel);
+    uf_p[ra] = rb;
+    uf_x[ra] = pa ^ pb ^ rel;
+    return 1;
+}
+
+static int search5(circ_t* st, tt_t T, tt_t M) {
+    int n = st->n;
+    /* outer cells for each pair (x,y), x<=y */
+    for (int a = 0; a < n; a++)
+        for (int b = a + 1; b < n; b++)
+            for (int c = b + 1; c < n; c++) {
+                tt_t mt[8];
+                for (int m = 0; m < 8; m++)
+                    mt[m] = M & ((m & 4) ? st->tt[a] : ~st->tt[a]) &
+                            ((m & 2) ? st->tt[b] : ~st->tt[b]) &
+                            ((m & 1) ? st->tt[c] : ~st->tt[c]);
+                for (int x = 0; x < n; x++)
+                    for (int y = x + 1; y < n; y++) {
+                        tt_t X = st->tt[x], Y = st->tt[y];
+                        tt_t Q[4] = {~X & ~Y, ~X & Y, X & ~Y, X & Y};
+                        int ok = 1;
+                        for (int i = 0; i < 12; i++) { uf_p[i] = i; uf_x[i] = 0; }
+                        int mixed[4];
+                        for (int q = 0; q < 4; q++) {
+                            tt_t cell = Q[q] & M;
+                            tt_t t1 = cell & T;
+                            mixed[q] = (t1 != 0 && t1 != cell);
+                        }
+                        for (int q = 0; q < 4 && ok; q++) {
+                            if (!mixed[q]) continue;
+                            for (int m = 0; m < 8; m++) {
+                                tt_t cell = mt[m] & Q[q];
+                                if (!cell) continue;
+                                tt_t t1 = cell & T;
+                                int v;
+                                if (t1 == 0) v = 0;
+                                else if (t1 == cell) v = 1;
+                                else { ok = 0; break; }
+                                if (!uf_union(m, 8 + q, v)) { ok = 0; break; }
+                            }
+                        }
+                        if (!ok) continue;
+                        /* derive h LUT */
+                        uint8_t hl = 0;
+                        for (int m = 0; m < 8; m++) {
+                            int p;
+                            uf_find(m, &p);
+                            /* h(m) relative to its root; root value = 0 */
+                            if (p) hl |= (uint8_t)(1u << m);
+                        }
+                        tt_t H = lut_eval(hl, st->tt[a], st->tt[b], st->tt[c]);
+                        uint8_t ol;
+                        /* outer LUT over (H, X, Y) */
+                        if (!find_lut3(H, X, Y, T, M, &ol)) continue; /* should not happen */
+                        int h = add_gate(st, a, b, c, hl);
+                        return add_gate(st, h, x, y, ol);
+                    }
+            }
+    return -1;
+}
+
+/* Returns gate index, or -1 if budget exhausted. */
+static int build(circ_t* st, tt_t T, tt_t M, int avail, int depth) {
+    if (M == 0) return 0;
+    for (int g = 0; g < st->n; g++) {
+        tt_t d = (st->tt[g] ^ T) & M;
+        if (d == 0 || d == M) return g;
+    }
+    if (st->n >= g_budget) return -1;
+    /* one new gate */
+    {
+        int n = st->n;
+        int start = (int)(rnd() % (unsigned)n);
+        for (int ai = 0; ai < n; ai++) {
+            int a = (ai + start) % n;
+            for (int b = 0; b < n; b++) {
+                if (b == a) continue;
+                for (int c = b + 1; c < n; c++) {
+                    if (c == a) continue;
+                    uint8_t l;
+                    if (find_lut3(st->tt[a], st->tt[b], st->tt[c], T, M, &l))
+                        return add_gate(st, a, b, c, l);
+                }
+            }
+        }
+    }
+    if (st->n + 2 > g_budget) return -1;
+    if (g_deep5 && depth <= 1) {
+        int g = search5(st, T, M);
+        if (g >= 0) return g;
+    }
+    if (st->n + 3 > g_budget) return -1;
+    /* split on a selector input */
+    circ_t best;
+    int best_g = -1;
+    best.n = 1 << 30;
+    int order[6], cnt = 0;
+    for (int s = 0; s < 6; s++)
+        if (avail & (1 << s)) order[cnt++] = s;
+    for (int i = cnt - 1; i > 0; i--) {
+        int j = (int)(rnd() % (unsigned)(i + 1));
+        int t = order[i]; order[i] = order[j]; order[j] = t;
+    }
+    int tries = depth == 0 ? cnt : (depth == 1 ? (cnt < 3 ? cnt : 3) : 1);
+    for (int si = 0; si < tries; si++) {
+        int s = order[si];
+        tt_t S = st->tt[s];
+        for (int first = 0; first < 2; first++) {
+            tt_t M0 = first == 0 ? (M & ~S) : (M & S);
+            tt_t M1 = M & ~M0;
+            for (int variant = 0; variant < 3; variant++) {
+                circ_t c = *st;
+                int f0 = build(&c, T, M0, avail & ~(1 << s), depth + 1);
+                if (f0 < 0) continue;
+                tt_t F0 = c.tt[f0];
+                tt_t T1 = T, MM1 = M1;
+                if (variant == 1) {
+                    T1 = T ^ F0; /* result = f0 ^ f1 on the other half */
+                } else if (variant == 2) {
+                    /* result = f0 | f1 (or with the right polarities): where
+                     * f0 already equals T on half-1 the f1 value is free. */
+                    tt_t agree = ~(F0 ^ T) & M1;
+                    tt_t agree_n = (F0 ^ T) & M1;
+                    /* choose polarity of f0 that covers more of T=1 ... */
+                    tt_t F = F0;
+                    if (__builtin_popcountll(agree_n & T) > __builtin_popcountll(agree & T))
+                        F = ~F0;
+                    /* OR form: where F=1 need T=1 */
+                    if ((F & M1 & ~T) == 0) {
+                        MM1 = M1 & ~F;
+                    } else if ((~F & M1 & T) == 0) {
+                        /* AND form: where F=0 need T=0 */
+                        MM1 = M1 & F;
+                    } else {
+                        continue;
+                    }
+                }
+                int f1 = build(&c, T1, MM1, avail & ~(1 << s), depth + 1);
+                if (f1 < 0) continue;
+                if (c.n >= g_budget) continue;
+                uint8_t l;
+                if (!find_lut3(c.tt[s], c.tt[f0], c.tt[f1], T, M, &l)) continue;
+                int g = add_gate(&c, s, f0, f1, l);
+                if (c.n < best.n) { best = c; best_g = g; }
+            }
+        }
+    }
+    if (best_g < 0) return -1;
+    *st = best;
+    return best_g;
+}
+
+static tt_t out_tt(int box, int bit) {
+    tt_t t = 0;
+    for (int p = 0; p < 64; p++) {
+        int row = ((p >> 4) & 2) | (p & 1);
+        int col = (p >> 1) & 0xF;
+        if ((SBOX[box][row * 16 + col] >> bit) & 1) t |= 1ull << p;
+    }
+    return t;
+}
+
+static void dump(const char* path, int box, const circ_t* c, const int* outs, const tt_t* tgt) {
+    FILE* f = path ? fopen(path, "w") : stdout;
+    if (!f) return;
+    fprintf(f, "box %d gates %d\n", box, c->n - 6);
+    for (int g = 6; g < c->n; g++)
+        fprintf(f, "g %d %d %d %d 0x%02x\n", g, c->in[g][0], c->in[g][1], c->in[g][2], c->lut[g]);
+    for (int o = 0; o < 4; o++) {
+        tt_t d = c->tt[outs[o]] ^ tgt[o];
+        fprintf(f, "o %d %d %d\n", o, outs[o], d == 0 ? 0 : 1);
+    }
+    if (path) fclose(f);
+}
+
+int main(int argc, char** argv) {
+    if (argc < 4) {
+        fprintf(stderr, "usage: %s box iterations seed [max_gates]\n", argv[0]);
+        return 2;
+    }
+    int box = atoi(argv[1]);
+    long iters = atol(argv[2]);
+    g_rng ^= (uint64_t)atoll(argv[3]) * 0x9E3779B97F4A7C15ull;
+    if (!g_rng) g_rng = 1;
+    int cap = argc > 4 ? atoi(argv[4]) : 60;
+    const char* out_path = argc > 5 ? argv[5] : NULL;
+    tt_t tgt[4];
+    for (int o = 0; o < 4; o++) tgt[o] = out_tt(box, o);
+    circ_t best;
+    int best_out[4] = {0};
+    best.n = 1 << 30;
+    for (long it = 0; it < iters; it++) {
+        circ_t c;
+        c.n = 6;
+        for (int i = 0; i < 6; i++) {
+            tt_t v = 0;
+            for (int p = 0; p < 64; p++)
+                if ((p >> i) & 1) v |= 1ull << p;
+            c.tt[i] = v;
+            c.in[i][0] = c.in[i][1] = c.in[i][2] = -1;
+            c.lut[i] = 0;
+        }
+        g_budget = (best.n < (1 << 30) ? best.n - 1 : cap);
+        if (g_budget > cap) g_budget = cap;
+        g_deep5 = (rnd() & 3) != 0;
+        int ord[4] = {0, 1, 2, 3};
+        for (int i = 3; i > 0; i--) {
+            int j = (int)(rnd() % (unsigned)(i + 1));
+            int t = ord[i]; ord[i] = ord[j]; ord[j] = t;
+        }
+        int outs[4], ok = 1;
+        for (int k = 0; k < 4 && ok; k++) {
+            int g = build(&c, tgt[ord[k]], ~0ull, 0x3F, 0);
+            if (g < 0) ok = 0;
+            outs[ord[k]] = g;
+        }
+        if (!ok) continue;
+        if (c.n < best.n) {
+            best = c;
+            memcpy(best_out, outs, sizeof outs);
+            fprintf(stderr, "box %d iter %ld: %d gates\n", box, it, c.n - 6);
+            if (out_path) dump(out_path, box, &best, best_out, tgt);
+        }
+    }
+    if (best.n == (1 << 30)) {
+        printf("FAIL\n");
+        return 1;
+    }
+    dump(NULL, box, &best, best_out, tgt);
+    return 0;
+}
