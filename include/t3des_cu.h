@@ -124,9 +124,10 @@ int t3des_cu_fill_splitmix(t3des_cu_ctx* ctx, void* dptr, uint64_t first_block, 
                            uint64_t seed, void* stream);
 
 /* Shard-additive, order-sensitive checksum of nblocks device blocks whose
- * global index starts at first_block; synchronous, result in *out. */
+ * global index starts at first_block.  Runs on `stream` (ordered after the
+ * work that produced dptr) and synchronises it; result in *out. */
 int t3des_cu_checksum(t3des_cu_ctx* ctx, const void* dptr, uint64_t first_block, size_t nblocks,
-                      uint64_t* out);
+                      uint64_t* out, void* stream);
 
 /* Number of cipher kernels this context has launched (for bench.py's
  * gpu_launches count). */

@@ -50,7 +50,7 @@ SIGNATURES = {
     "t3des_cu_host_alloc": (_i, [_sz, ctypes.POINTER(_vp)]),
     "t3des_cu_host_free": (_i, [_vp]),
     "t3des_cu_fill_splitmix": (_i, [_vp, _vp, ctypes.c_uint64, _sz, ctypes.c_uint64, _vp]),
-    "t3des_cu_checksum": (_i, [_vp, _vp, ctypes.c_uint64, _sz, _u64p]),
+    "t3des_cu_checksum": (_i, [_vp, _vp, ctypes.c_uint64, _sz, _u64p, _vp]),
     "t3des_cu_launch_count": (_i, [_vp, _u64p]),
 }
 

@@ -202,9 +202,10 @@ class Engine:
     def fill_splitmix(self, dptr: int, first_block: int, nblocks: int, seed: int, stream: int = 0) -> None:
         _raise(self._lib.t3des_cu_fill_splitmix(self._h, dptr, first_block, nblocks, seed, stream or None))
 
-    def checksum(self, dptr: int, first_block: int, nblocks: int) -> int:
+    def checksum(self, dptr: int, first_block: int, nblocks: int, stream: int = 0) -> int:
+        """Checksum on `stream` (default: the legacy default stream)."""
         out = ctypes.c_uint64()
-        _raise(self._lib.t3des_cu_checksum(self._h, dptr, first_block, nblocks, ctypes.byref(out)))
+        _raise(self._lib.t3des_cu_checksum(self._h, dptr, first_block, nblocks, ctypes.byref(out), stream or None))
         return out.value
 
     def launch_count(self) -> int:

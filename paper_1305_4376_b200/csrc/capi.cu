@@ -374,10 +374,10 @@ int t3des_cu_fill_splitmix(t3des_cu_ctx* c, void* dptr, std::uint64_t first_bloc
 }
 
 int t3des_cu_checksum(t3des_cu_ctx* c, const void* dptr, std::uint64_t first_block, std::size_t nblocks,
-                      std::uint64_t* out) {
+                      std::uint64_t* out, void* stream) {
     if (!c || !out || (nblocks && !dptr)) return T3DES_CU_ERR_ARG;
     DeviceScope scope(c->device);
-    cudaStream_t s = c->st[0];
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
     unsigned long long h = 0;
     T3_CK(cudaMemsetAsync(c->d_acc, 0, sizeof h, s));
     if (nblocks) {
