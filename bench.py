@@ -203,7 +203,7 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--variant", choices=["bitslice", "sptable"], default="bitslice")
+    ap.add_argument("--variant", choices=["bitslice", "bitslice_ldg", "sptable"], default="bitslice")
     ap.add_argument("--gib", type=int, default=1, help="GiB per GPU per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -243,7 +243,8 @@ def main() -> None:
     e = t3.Engine(local)
     ts = t3.triple_schedule(t3.parse_hex_key(BENCH_KEY))
     e.set_schedule(ts)
-    e.set_variant(N.VARIANT_SPTABLE if args.variant == "sptable" else N.VARIANT_BITSLICE)
+    VARIANTS = {"bitslice": N.VARIANT_BITSLICE, "bitslice_ldg": N.VARIANT_BITSLICE_LDG, "sptable": N.VARIANT_SPTABLE}
+    e.set_variant(VARIANTS[args.variant])
     nblocks = (args.gib << 30) // 8
     nbytes = 8 * nblocks
     first_block = rank * nblocks
@@ -322,22 +323,25 @@ def main() -> None:
         "parity_sampled_vs_oracle": parity_ok,
     }
 
-    # secondary variant (north star: bitsliced vs SP-table, ncu picks)
+    # the other variants (north star: bitsliced vs SP-table, ncu picks)
     if not args.no_variants:
-        other = "sptable" if args.variant == "bitslice" else "bitslice"
-        e.set_variant(N.VARIANT_SPTABLE if other == "sptable" else N.VARIANT_BITSLICE)
-        for _ in range(2):
-            e.ecb_device(0, src.data_ptr(), dst.data_ptr(), nbytes, sp)
-        barrier()
-        k2 = max(3, args.steps // 4)
-        ev0.record(stream)
-        for _ in range(k2):
-            e.ecb_device(0, src.data_ptr(), dst.data_ptr(), nbytes, sp)
-        ev1.record(stream)
-        barrier()
-        ms2 = max_over_ranks(ev0.elapsed_time(ev1) / k2)
-        line["variants"] = {args.variant: round(gbs, 3), other: round(world * nbytes / (ms2 * 1e-3) / 1e9, 3)}
-        e.set_variant(N.VARIANT_SPTABLE if args.variant == "sptable" else N.VARIANT_BITSLICE)
+        line["variants"] = {args.variant: round(gbs, 3)}
+        for other, code in VARIANTS.items():
+            if other == args.variant:
+                continue
+            e.set_variant(code)
+            for _ in range(2):
+                e.ecb_device(0, src.data_ptr(), dst.data_ptr(), nbytes, sp)
+            barrier()
+            k2 = max(3, args.steps // 4)
+            ev0.record(stream)
+            for _ in range(k2):
+                e.ecb_device(0, src.data_ptr(), dst.data_ptr(), nbytes, sp)
+            ev1.record(stream)
+            barrier()
+            ms2 = max_over_ranks(ev0.elapsed_time(ev1) / k2)
+            line["variants"][other] = round(world * nbytes / (ms2 * 1e-3) / 1e9, 3)
+        e.set_variant(VARIANTS[args.variant])
 
     del dst
     torch.cuda.empty_cache()

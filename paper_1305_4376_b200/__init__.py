@@ -7,6 +7,7 @@ from ._native import (  # noqa: F401
     DECRYPT,
     ENCRYPT,
     VARIANT_BITSLICE,
+    VARIANT_BITSLICE_LDG,
     VARIANT_SPTABLE,
     EngineUnavailable,
     LIB_PATH,

@@ -80,7 +80,9 @@ int launch_bitslice(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8
         grid = std::min<std::uint64_t>(grid, std::max<std::uint64_t>(cap, 1));
         const bool vec4 = ((reinterpret_cast<std::uintptr_t>(in) |
                             reinterpret_cast<std::uintptr_t>(out)) & 15u) == 0;
-        if (vec4)
+        if (vec4 && c->variant == T3DES_CU_VARIANT_BITSLICE && threads == T3_BS_THREADS)
+            t3_bs_tma_kernel<<<unsigned(grid), threads, 0, s>>>(in, out, full, c->bs[dir]);
+        else if (vec4)
             t3_bs_kernel<4, false><<<unsigned(grid), threads, 0, s>>>(in, out, 0, full, nblocks, c->bs[dir]);
         else
             t3_bs_kernel<2, false><<<unsigned(grid), threads, 0, s>>>(in, out, 0, full, nblocks, c->bs[dir]);
@@ -195,8 +197,11 @@ int t3des_cu_create(int device, t3des_cu_ctx** out) {
     c->sms = prop.multiProcessorCount;
     int rc = T3DES_CU_OK;
     do {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->bs_occ, t3_bs_kernel<4, false>,
-                                                          T3_BS_THREADS, 0) != cudaSuccess) {
+        int occ_ldg = 1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->bs_occ, t3_bs_tma_kernel, T3_BS_THREADS, 0) !=
+                cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_ldg, t3_bs_kernel<4, false>, T3_BS_THREADS, 0) !=
+                cudaSuccess) {
             rc = T3DES_CU_ERR_CUDA;
             break;
         }
@@ -207,7 +212,7 @@ int t3des_cu_create(int device, t3des_cu_ctx** out) {
             rc = T3DES_CU_ERR_CUDA;
             break;
         }
-        c->bs_occ = std::max(c->bs_occ, 1);
+        c->bs_occ = std::max(std::min(c->bs_occ, occ_ldg), 1);
         c->sp_occ = std::max(c->sp_occ, 1);
         std::uint32_t sp[8][64];
         t3b::build_sp_tables(sp);
@@ -260,7 +265,8 @@ int t3des_cu_set_schedule(t3des_cu_ctx* c, const std::uint64_t sub48[48]) {
 }
 
 int t3des_cu_set_variant(t3des_cu_ctx* c, int variant) {
-    if (!c || (variant != T3DES_CU_VARIANT_BITSLICE && variant != T3DES_CU_VARIANT_SPTABLE))
+    if (!c || (variant != T3DES_CU_VARIANT_BITSLICE && variant != T3DES_CU_VARIANT_SPTABLE &&
+               variant != T3DES_CU_VARIANT_BITSLICE_LDG))
         return T3DES_CU_ERR_ARG;
     c->variant = variant;
     return T3DES_CU_OK;
@@ -268,7 +274,7 @@ int t3des_cu_set_variant(t3des_cu_ctx* c, int variant) {
 
 int t3des_cu_set_launch(t3des_cu_ctx* c, std::size_t chunk_blocks, int work_group) {
     if (!c || work_group < 0 || work_group > 1024 || (work_group % 32) != 0) return T3DES_CU_ERR_ARG;
-    if (work_group > T3_BS_THREADS && c->variant == T3DES_CU_VARIANT_BITSLICE) return T3DES_CU_ERR_ARG;
+    if (work_group > T3_BS_THREADS && c->variant != T3DES_CU_VARIANT_SPTABLE) return T3DES_CU_ERR_ARG;
     c->chunk_blocks = chunk_blocks;
     c->work_group = work_group;
     return T3DES_CU_OK;
