@@ -26,7 +26,6 @@ import argparse
 import ctypes
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -57,63 +56,59 @@ def measured_peaks() -> dict:
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle sampling during the timed region."""
+    """SM clock and throttle reasons sampled DURING the timed region via NVML
+    (every ~2 ms in a thread; nvidia-smi's 100 ms floor would see a 30 ms
+    region only once)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
 
     def __init__(self, device: int):
         self.device = device
-        self.proc = None
-        self.lines: list[str] = []
-        self.t = None
+        self.samples: list[tuple[float, float, int]] = []
+        self._stop = threading.Event()
+        self._t = None
+        self._nvml = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            import pynvml
+
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.device]) if vis else self.device
+            h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self._nvml = (pynvml, h)
+            self._t = threading.Thread(target=self._loop, daemon=True)
+            self._t.start()
         except Exception:
-            self.proc = None
+            self._nvml = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _loop(self):
+        pynvml, h = self._nvml
+        mx = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+        while not self._stop.is_set():
+            try:
+                sm = float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                rs = int(pynvml.nvmlDeviceGetCurrentClocksEventReasons(h))
+                self.samples.append((sm, mx, rs))
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
-            if self.t:
-                self.t.join(timeout=2)
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=2)
 
     def summary(self) -> dict:
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            p = [x.strip() for x in ln.split(",")]
-            if len(p) < 8:
-                continue
-            try:
-                sm.append(float(p[0]))
-                mx.append(float(p[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, p[4:8]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        sm_sorted = sorted(sm)
-        return {"sm_mhz": sm_sorted[len(sm_sorted) // 2], "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "source": "unavailable"}
+        sm = sorted(x[0] for x in self.samples)
+        reasons = sorted({n for _, _, r in self.samples for n, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(x[1] for x in self.samples), "sm_min_mhz": sm[0],
+                "reasons": reasons, "samples": len(sm), "source": "nvml"}
 
 
 def cpu_reference_arm(nbytes_target_s: float = 12.0):
@@ -245,9 +240,11 @@ def main() -> None:
     e.set_schedule(ts)
     VARIANTS = {"bitslice": N.VARIANT_BITSLICE, "bitslice_ldg": N.VARIANT_BITSLICE_LDG, "sptable": N.VARIANT_SPTABLE}
     e.set_variant(VARIANTS[args.variant])
-    nblocks = (args.gib << 30) // 8
+    from paper_1305_4376_b200.sharding import shard_range
+
+    per_rank = (args.gib << 30) // 8
+    first_block, nblocks = shard_range(world * per_rank, world, rank)  # == rank * per_rank
     nbytes = 8 * nblocks
-    first_block = rank * nblocks
     stream = torch.cuda.Stream()
     sp = stream.cuda_stream
     src = torch.empty(nbytes, dtype=torch.uint8, device="cuda")

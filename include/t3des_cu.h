@@ -113,6 +113,11 @@ int t3des_cu_ecb_host(t3des_cu_ctx* ctx, int direction, const uint8_t* in, uint8
 int t3des_cu_ecb_multi(const int* devices, int ndev, const uint64_t sub48[48], int direction,
                        const uint8_t* in, uint8_t* out, size_t len);
 
+/* The block range device `g` of `ndev` owns in t3des_cu_ecb_multi (and in
+ * bench.py's torchrun ranks): [first, first + count), boundaries at
+ * floor(g*N/ndev) rounded down to 1024-block tiles; the last shard ends at N. */
+int t3des_cu_shard_range(uint64_t nblocks, int ndev, int g, uint64_t* first, uint64_t* count);
+
 /* ---- utilities --------------------------------------------------------- */
 
 /* Pinned host memory for t3des_cu_ecb_host. */

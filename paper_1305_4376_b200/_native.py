@@ -48,6 +48,7 @@ SIGNATURES = {
     "t3des_cu_ecb_device": (_i, [_vp, _i, _vp, _vp, _sz, _vp]),
     "t3des_cu_ecb_host": (_i, [_vp, _i, _vp, _vp, _sz]),
     "t3des_cu_ecb_multi": (_i, [ctypes.POINTER(_i), _i, _u64p, _i, _vp, _vp, _sz]),
+    "t3des_cu_shard_range": (_i, [ctypes.c_uint64, _i, _i, _u64p, _u64p]),
     "t3des_cu_host_alloc": (_i, [_sz, ctypes.POINTER(_vp)]),
     "t3des_cu_host_free": (_i, [_vp]),
     "t3des_cu_fill_splitmix": (_i, [_vp, _vp, ctypes.c_uint64, _sz, ctypes.c_uint64, _vp]),

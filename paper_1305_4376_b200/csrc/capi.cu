@@ -320,6 +320,20 @@ int t3des_cu_ecb_host(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uin
     return T3DES_CU_OK;
 }
 
+int t3des_cu_shard_range(std::uint64_t nblocks, int ndev, int g, std::uint64_t* first, std::uint64_t* count) {
+    if (ndev <= 0 || g < 0 || g >= ndev || !first || !count) return T3DES_CU_ERR_ARG;
+    auto cut = [&](int k) -> std::uint64_t {
+        if (k >= ndev) return nblocks;
+        // 128-bit product: nblocks * k may exceed 2^64 for huge inputs
+        const unsigned __int128 p = static_cast<unsigned __int128>(nblocks) * static_cast<unsigned>(k);
+        std::uint64_t b = static_cast<std::uint64_t>(p / static_cast<unsigned>(ndev));
+        return b - b % T3_TILE_BLOCKS;
+    };
+    *first = cut(g);
+    *count = cut(g + 1) - *first;
+    return T3DES_CU_OK;
+}
+
 int t3des_cu_ecb_multi(const int* devices, int ndev, const std::uint64_t sub48[48], int dir,
                        const std::uint8_t* in, std::uint8_t* out, std::size_t len) {
     if (!devices || ndev <= 0 || !sub48 || (dir != 0 && dir != 1)) return T3DES_CU_ERR_ARG;
@@ -328,18 +342,13 @@ int t3des_cu_ecb_multi(const int* devices, int ndev, const std::uint64_t sub48[4
     if (partial_overlap(in, out, len)) return T3DES_CU_ERR_OVERLAP;
     if (!len) return T3DES_CU_OK;
     const std::uint64_t nblocks = len / 8;
-    // Contiguous shards [g*N/G, (g+1)*N/G) rounded down to whole tiles.
-    std::vector<std::uint64_t> cut(ndev + 1);
-    for (int g = 0; g <= ndev; ++g) {
-        std::uint64_t b = nblocks * std::uint64_t(g) / std::uint64_t(ndev);
-        if (g < ndev) b -= b % T3_TILE_BLOCKS;
-        cut[g] = g == ndev ? nblocks : b;
-    }
     std::vector<int> rcs(ndev, T3DES_CU_OK);
     std::vector<std::thread> workers;
     for (int g = 0; g < ndev; ++g) {
         workers.emplace_back([&, g] {
-            const std::uint64_t b0 = cut[g], b1 = cut[g + 1];
+            std::uint64_t b0 = 0, cnt = 0;
+            t3des_cu_shard_range(nblocks, ndev, g, &b0, &cnt);
+            const std::uint64_t b1 = b0 + cnt;
             if (b1 <= b0) return;
             t3des_cu_ctx* c = nullptr;
             int rc = t3des_cu_create(devices[g], &c);

@@ -1,0 +1,92 @@
+"""Multi-GPU decomposition, exercised on CPU with world-size-2 gloo (no GPU
+here): each rank takes its shard (t3des_cu_shard_range, the same function the
+C ABI's ecb_multi and bench.py's ranks use), transforms it with the CPU
+oracle as a stand-in for its device, and the ranks check that the shards
+tile the stream exactly, that concatenating them equals the single-process
+result, that the shard checksums add up (the invariant the GPU runs check
+across 1/2/4/8 GPUs), and that the max-over-ranks timing reduction works."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1305_4376_b200.sharding import TILE_BLOCKS, shard_range
+from tests.oracle_util import Oracle, checksum
+
+KEY = "133457799BBCDFF10E329232EA6D0D737CA110454A1A6E57"
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank: int, world: int, port: int, nblocks: int, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        o = Oracle.load()
+        s = o.schedule_hex(KEY)
+        first, count = shard_range(nblocks, world, rank)
+        x = o.splitmix(first, count, 0x3DE5C0DE)
+        y = o.ecb(x, s, 0, threads=1)
+        cs = torch.tensor([checksum(y, first) & ((1 << 63) - 1), checksum(y, first) >> 63], dtype=torch.int64)
+        dist.all_reduce(cs, op=dist.ReduceOp.SUM)
+        bounds = torch.tensor([first, count], dtype=torch.int64)
+        gathered = [torch.zeros(2, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(gathered, bounds)
+        outs = [None] * world
+        dist.all_gather_object(outs, y.tobytes())
+        t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        if rank == 0:
+            q.put((cs.tolist(), [g.tolist() for g in gathered], b"".join(outs), float(t.item())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("nblocks", [0, 1, 1023, 5 * TILE_BLOCKS + 17, 65536])
+def test_two_rank_block_range_sharding(nblocks):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, nblocks, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    cs, bounds, joined, tmax = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    # shards tile [0, N) in order, boundaries on 1024-block tiles
+    pos = 0
+    for first, count in bounds:
+        assert first == pos
+        pos += count
+    assert pos == nblocks
+    assert all(f % TILE_BLOCKS == 0 for f, _ in bounds)
+    o = Oracle.load()
+    whole = o.ecb(o.splitmix(0, nblocks, 0x3DE5C0DE), o.schedule_hex(KEY), 0)
+    assert joined == whole.tobytes()
+    full = checksum(whole, 0)
+    assert ((cs[1] << 63) + cs[0]) % 2**64 == full
+    assert tmax == 2.0
+
+
+def test_shard_range_properties():
+    for n in (0, 1, 1024, 10**6 + 3, 8_589_934_592):
+        for world in (1, 2, 4, 8):
+            spans = [shard_range(n, world, g) for g in range(world)]
+            assert spans[0][0] == 0
+            assert sum(c for _, c in spans) == n
+            for (f0, c0), (f1, _) in zip(spans, spans[1:]):
+                assert f0 + c0 == f1 and f1 % TILE_BLOCKS == 0
+    # 64 GiB over 8 GPUs: exactly 8 GiB each (BASELINE configs[3])
+    assert shard_range(8_589_934_592, 8, 3) == (3 * 1_073_741_824, 1_073_741_824)
+    with pytest.raises(ValueError):
+        shard_range(10, 2, 2)
