@@ -48,6 +48,7 @@ extern "C" {
 #define T3DES_CU_VARIANT_BITSLICE 0     /* bitsliced lop3 kernel, TMA tile prefetch (default) */
 #define T3DES_CU_VARIANT_SPTABLE 1      /* shared-memory SP-table kernel                      */
 #define T3DES_CU_VARIANT_BITSLICE_LDG 2 /* bitsliced, direct LDG loads (kept for measurement) */
+#define T3DES_CU_VARIANT_BITSLICE_ALU 3 /* bitsliced + TMA, all-ALU round (kept for measurement) */
 
 typedef struct t3des_cu_ctx t3des_cu_ctx;
 

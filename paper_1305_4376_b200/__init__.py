@@ -8,6 +8,7 @@ from ._native import (  # noqa: F401
     ENCRYPT,
     VARIANT_BITSLICE,
     VARIANT_BITSLICE_LDG,
+    VARIANT_BITSLICE_ALU,
     VARIANT_SPTABLE,
     EngineUnavailable,
     LIB_PATH,

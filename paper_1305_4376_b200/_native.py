@@ -28,6 +28,7 @@ DECRYPT = 1
 VARIANT_BITSLICE = 0
 VARIANT_SPTABLE = 1
 VARIANT_BITSLICE_LDG = 2
+VARIANT_BITSLICE_ALU = 3
 
 # Every symbol include/t3des_cu.h declares: name -> (restype, argtypes).
 _u64p = ctypes.POINTER(ctypes.c_uint64)

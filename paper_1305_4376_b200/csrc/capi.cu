@@ -80,8 +80,12 @@ int launch_bitslice(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8
         grid = std::min<std::uint64_t>(grid, std::max<std::uint64_t>(cap, 1));
         const bool vec4 = ((reinterpret_cast<std::uintptr_t>(in) |
                             reinterpret_cast<std::uintptr_t>(out)) & 15u) == 0;
-        if (vec4 && c->variant == T3DES_CU_VARIANT_BITSLICE && threads == T3_BS_THREADS)
-            t3_bs_tma_kernel<<<unsigned(grid), threads, 0, s>>>(in, out, full, c->bs[dir]);
+        const bool tma = vec4 && threads == T3_BS_THREADS &&
+                         (c->variant == T3DES_CU_VARIANT_BITSLICE || c->variant == T3DES_CU_VARIANT_BITSLICE_ALU);
+        if (tma && c->variant == T3DES_CU_VARIANT_BITSLICE_ALU)
+            t3_bs_tma_kernel<false><<<unsigned(grid), threads, 0, s>>>(in, out, full, c->bs[dir]);
+        else if (tma)
+            t3_bs_tma_kernel<true><<<unsigned(grid), threads, 0, s>>>(in, out, full, c->bs[dir]);
         else if (vec4)
             t3_bs_kernel<4, false><<<unsigned(grid), threads, 0, s>>>(in, out, 0, full, nblocks, c->bs[dir]);
         else
@@ -198,7 +202,7 @@ int t3des_cu_create(int device, t3des_cu_ctx** out) {
     int rc = T3DES_CU_OK;
     do {
         int occ_ldg = 1;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->bs_occ, t3_bs_tma_kernel, T3_BS_THREADS, 0) !=
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->bs_occ, t3_bs_tma_kernel<true>, T3_BS_THREADS, 0) !=
                 cudaSuccess ||
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_ldg, t3_bs_kernel<4, false>, T3_BS_THREADS, 0) !=
                 cudaSuccess) {
@@ -265,8 +269,7 @@ int t3des_cu_set_schedule(t3des_cu_ctx* c, const std::uint64_t sub48[48]) {
 }
 
 int t3des_cu_set_variant(t3des_cu_ctx* c, int variant) {
-    if (!c || (variant != T3DES_CU_VARIANT_BITSLICE && variant != T3DES_CU_VARIANT_SPTABLE &&
-               variant != T3DES_CU_VARIANT_BITSLICE_LDG))
+    if (!c || variant < T3DES_CU_VARIANT_BITSLICE || variant > T3DES_CU_VARIANT_BITSLICE_ALU)
         return T3DES_CU_ERR_ARG;
     c->variant = variant;
     return T3DES_CU_OK;

@@ -144,11 +144,12 @@ void build_bitslice_table(const std::uint64_t seq[48], T3BsTable& tab) {
                 wh[rh][q] = want;
             }
         }
-        std::uint32_t* rk = tab.w + T3_TAB_ROUND + 48 * t;
+        std::uint32_t* rk = tab.w + T3_TAB_ROUND + T3_ROUND_WORDS * t;
         for (int d = 0; d < 16; ++d) {
             const int j = T3_SECONDARY_SLOT[d];
             const int q = T3_E[j] - 1;
             rk[32 + d] = kbit(seq[t], j) ^ wh[rh][q];
+            rk[48 + d] = rk[32 + d] | 1u;  // multiplier of the FMA form
         }
         std::uint32_t nxt[32];
         target_after(lh, t, nxt);

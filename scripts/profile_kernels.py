@@ -18,7 +18,8 @@ s = torch.cuda.current_stream().cuda_stream
 e.fill_splitmix(src.data_ptr(), 0, n, 0x3DE5C0DE, s)
 variants = sys.argv[1:] or ["bitslice", "sptable"]
 for v in variants:
-    e.set_variant(t3.VARIANT_SPTABLE if v == "sptable" else t3.VARIANT_BITSLICE)
+    e.set_variant({"sptable": t3.VARIANT_SPTABLE, "bitslice_ldg": t3.VARIANT_BITSLICE_LDG,
+                   "bitslice_alu": t3.VARIANT_BITSLICE_ALU}.get(v, t3.VARIANT_BITSLICE))
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     for i in range(3):
         ev[0].record()

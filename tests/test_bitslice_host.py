@@ -70,9 +70,10 @@ def test_whitening_table_primary_slots(oracle):
     Re-simulate the kernel's XOR sequence symbolically from the table."""
     lib = bs_host()
     s = oracle.schedule_hex(KEYS[0])
-    w = (ctypes.c_uint32 * 2496)()
-    lib.bs_host_table(s, 0, w)
-    w = np.frombuffer(w, dtype=np.uint32).astype(np.uint64) & 1
+    w = (ctypes.c_uint32 * 8192)()
+    nw = lib.bs_host_table(s, 0, w)
+    stride = (nw - 64 - 128) // 48  # words per round
+    w = np.array(w[:nw], dtype=np.uint64) & 1
     seq = [s[i] for i in range(16)] + [s[31 - i] for i in range(16)] + [s[32 + i] for i in range(16)]
     prim = G.e_slot_maps()[0]
 
@@ -85,13 +86,13 @@ def test_whitening_table_primary_slots(oracle):
         lh = (loc % 2) if p != 1 else 1 - (loc % 2)
         rh = 1 - lh
         if t == 16:
-            wh[0] ^= w[2368:2400]
+            wh[0] ^= w[nw - 128: nw - 96]
         if t == 32:
-            wh[1] ^= w[2400:2432]
+            wh[1] ^= w[nw - 96: nw - 64]
         assert np.array_equal(wh[rh], kp(t)), t
-        wh[lh] ^= w[64 + 48 * t: 64 + 48 * t + 32]
-    wh[0] ^= w[2432:2464]
-    wh[1] ^= w[2464:2496]
+        wh[lh] ^= w[64 + stride * t: 64 + stride * t + 32]
+    wh[0] ^= w[nw - 64: nw - 32]
+    wh[1] ^= w[nw - 32: nw]
     assert not wh[0].any() and not wh[1].any()
 
 
