@@ -198,7 +198,7 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--variant", choices=["bitslice", "bitslice_alu", "bitslice_ldg", "sptable"], default="bitslice")
+    ap.add_argument("--variant", choices=["bitslice", "bitslice_alu", "bitslice_dfma", "bitslice_shrfma", "bitslice_ldg", "sptable"], default="bitslice")
     ap.add_argument("--gib", type=int, default=1, help="GiB per GPU per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -239,6 +239,7 @@ def main() -> None:
     ts = t3.triple_schedule(t3.parse_hex_key(BENCH_KEY))
     e.set_schedule(ts)
     VARIANTS = {"bitslice": N.VARIANT_BITSLICE, "bitslice_alu": N.VARIANT_BITSLICE_ALU,
+                "bitslice_dfma": N.VARIANT_BITSLICE_DFMA, "bitslice_shrfma": N.VARIANT_BITSLICE_SHRFMA,
                 "bitslice_ldg": N.VARIANT_BITSLICE_LDG, "sptable": N.VARIANT_SPTABLE}
     e.set_variant(VARIANTS[args.variant])
     from paper_1305_4376_b200.sharding import shard_range

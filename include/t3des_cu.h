@@ -48,7 +48,10 @@ extern "C" {
 #define T3DES_CU_VARIANT_BITSLICE 0     /* bitsliced lop3 kernel, TMA tile prefetch (default) */
 #define T3DES_CU_VARIANT_SPTABLE 1      /* shared-memory SP-table kernel                      */
 #define T3DES_CU_VARIANT_BITSLICE_LDG 2 /* bitsliced, direct LDG loads (kept for measurement) */
-#define T3DES_CU_VARIANT_BITSLICE_ALU 3 /* bitsliced + TMA, all-ALU round (kept for measurement) */
+/* Tuning variants of the bitsliced + TMA kernel (A/B measurement only):   */
+#define T3DES_CU_VARIANT_BITSLICE_ALU 3    /* all key/shift work on the ALU pipe    */
+#define T3DES_CU_VARIANT_BITSLICE_DFMA 4   /* E-duplicate key XORs as IMAD          */
+#define T3DES_CU_VARIANT_BITSLICE_SHRFMA 5 /* transpose right shifts as IMAD.HI     */
 
 typedef struct t3des_cu_ctx t3des_cu_ctx;
 

@@ -9,6 +9,8 @@ from ._native import (  # noqa: F401
     VARIANT_BITSLICE,
     VARIANT_BITSLICE_LDG,
     VARIANT_BITSLICE_ALU,
+    VARIANT_BITSLICE_DFMA,
+    VARIANT_BITSLICE_SHRFMA,
     VARIANT_SPTABLE,
     EngineUnavailable,
     LIB_PATH,

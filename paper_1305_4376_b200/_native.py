@@ -29,6 +29,8 @@ VARIANT_BITSLICE = 0
 VARIANT_SPTABLE = 1
 VARIANT_BITSLICE_LDG = 2
 VARIANT_BITSLICE_ALU = 3
+VARIANT_BITSLICE_DFMA = 4
+VARIANT_BITSLICE_SHRFMA = 5
 
 # Every symbol include/t3des_cu.h declares: name -> (restype, argtypes).
 _u64p = ctypes.POINTER(ctypes.c_uint64)

@@ -80,12 +80,18 @@ int launch_bitslice(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8
         grid = std::min<std::uint64_t>(grid, std::max<std::uint64_t>(cap, 1));
         const bool vec4 = ((reinterpret_cast<std::uintptr_t>(in) |
                             reinterpret_cast<std::uintptr_t>(out)) & 15u) == 0;
-        const bool tma = vec4 && threads == T3_BS_THREADS &&
-                         (c->variant == T3DES_CU_VARIANT_BITSLICE || c->variant == T3DES_CU_VARIANT_BITSLICE_ALU);
-        if (tma && c->variant == T3DES_CU_VARIANT_BITSLICE_ALU)
-            t3_bs_tma_kernel<false><<<unsigned(grid), threads, 0, s>>>(in, out, full, c->bs[dir]);
+        const bool tma = vec4 && threads == T3_BS_THREADS && c->variant != T3DES_CU_VARIANT_BITSLICE_LDG;
+        // tuning variants (A/B measurement of the T3_OPT_* code-generation options)
+        const int opt = c->variant == T3DES_CU_VARIANT_BITSLICE ? T3_OPT_DEFAULT
+                        : c->variant == T3DES_CU_VARIANT_BITSLICE_ALU ? 0
+                        : c->variant == T3DES_CU_VARIANT_BITSLICE_DFMA ? T3_OPT_DFMA
+                                                                       : T3_OPT_SHRFMA;
+        if (tma && opt == 0)
+            t3_bs_tma_kernel<0><<<unsigned(grid), threads, 0, s>>>(in, out, full, c->bs[dir]);
+        else if (tma && opt == T3_OPT_DFMA)
+            t3_bs_tma_kernel<T3_OPT_DFMA><<<unsigned(grid), threads, 0, s>>>(in, out, full, c->bs[dir]);
         else if (tma)
-            t3_bs_tma_kernel<true><<<unsigned(grid), threads, 0, s>>>(in, out, full, c->bs[dir]);
+            t3_bs_tma_kernel<T3_OPT_SHRFMA><<<unsigned(grid), threads, 0, s>>>(in, out, full, c->bs[dir]);
         else if (vec4)
             t3_bs_kernel<4, false><<<unsigned(grid), threads, 0, s>>>(in, out, 0, full, nblocks, c->bs[dir]);
         else
@@ -202,7 +208,7 @@ int t3des_cu_create(int device, t3des_cu_ctx** out) {
     int rc = T3DES_CU_OK;
     do {
         int occ_ldg = 1;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->bs_occ, t3_bs_tma_kernel<true>, T3_BS_THREADS, 0) !=
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->bs_occ, t3_bs_tma_kernel<T3_OPT_DEFAULT>, T3_BS_THREADS, 0) !=
                 cudaSuccess ||
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_ldg, t3_bs_kernel<4, false>, T3_BS_THREADS, 0) !=
                 cudaSuccess) {
@@ -269,7 +275,7 @@ int t3des_cu_set_schedule(t3des_cu_ctx* c, const std::uint64_t sub48[48]) {
 }
 
 int t3des_cu_set_variant(t3des_cu_ctx* c, int variant) {
-    if (!c || variant < T3DES_CU_VARIANT_BITSLICE || variant > T3DES_CU_VARIANT_BITSLICE_ALU)
+    if (!c || variant < T3DES_CU_VARIANT_BITSLICE || variant > T3DES_CU_VARIANT_BITSLICE_SHRFMA)
         return T3DES_CU_ERR_ARG;
     c->variant = variant;
     return T3DES_CU_OK;

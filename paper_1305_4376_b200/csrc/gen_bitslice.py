@@ -143,7 +143,7 @@ def gen_round(circuits) -> list[str]:
     out.append("//   k[0..31]  : C, XORed into L bit p together with f bit p")
     out.append("//   k[32..47] : D, XORed into the 16 duplicated E slots")
     out.append("//   k[48..63] : S = D | 1, for the FMA-pipe form x ^ D = x * S + D")
-    out.append("template <bool FMA, class KP>")
+    out.append("template <int OPT, class KP>")
     out.append("T3_FI void t3_round(uint32_t (&L)[32], const uint32_t (&R)[32], const KP k) {")
     for box in range(8):
         gates, outs = circuits[box]
@@ -154,7 +154,7 @@ def gen_round(circuits) -> list[str]:
             q = E[j] - 1
             if j in d_index:
                 nm = f"x{kvar}"
-                out.append(f"    const uint32_t {nm} = t3_dfix<FMA>(R[{q}], k[{32 + d_index[j]}], k[{48 + d_index[j]}]);")
+                out.append(f"    const uint32_t {nm} = t3_dfix<OPT>(R[{q}], k[{32 + d_index[j]}], k[{48 + d_index[j]}]);")
                 names[kvar] = nm
             else:
                 names[kvar] = f"R[{q}]"

@@ -24,6 +24,9 @@
 #define T3_BS_MIN_CTAS 4
 #define T3_SP_THREADS 256
 #define T3_TILE_BLOCKS 1024  // blocks per warp tile (32 lanes x 32 blocks)
+#ifndef T3_OPT_DEFAULT
+#define T3_OPT_DEFAULT 0
+#endif
 
 struct T3SpKeyParam {
     uint32_t k[48][8];
@@ -35,7 +38,7 @@ struct T3SpKeyParam {
 // VEC = 2: lane t loads block 32k + t, k < 32, with LDG.64.
 // TAIL:    the final partial tile; missing blocks read as zero and are not
 //          stored (only VEC = 2).
-template <int VEC, bool TAIL, bool FMA = true>
+template <int VEC, bool TAIL, int OPT = T3_OPT_DEFAULT>
 __global__ void __launch_bounds__(T3_BS_THREADS, T3_BS_MIN_CTAS)
 t3_bs_kernel(const uint8_t* in, uint8_t* out, uint64_t first_tile, uint64_t ntiles,
              uint64_t nblocks, const __grid_constant__ T3BsTable tab) {
@@ -65,7 +68,7 @@ t3_bs_kernel(const uint8_t* in, uint8_t* out, uint64_t first_tile, uint64_t ntil
                 hi[k] = v.y;
             }
         }
-        t3_tile32<FMA>(lo, hi, tab.w);
+        t3_tile32<OPT>(lo, hi, tab.w);
         if (VEC == 4) {
             uint4* dst = reinterpret_cast<uint4*>(out + base * 8) + lane;
 #pragma unroll
@@ -81,9 +84,8 @@ t3_bs_kernel(const uint8_t* in, uint8_t* out, uint64_t first_tile, uint64_t ntil
 }
 
 // ---- bitsliced kernel with TMA prefetch (aligned full tiles) ----------
-// FMA = true moves the E-duplicate key corrections and the transposes'
-// right shifts from the saturated ALU pipe to the idle FMA pipe (IMAD,
-// IMAD.HI); FMA = false keeps the all-LOP3 form (T3DES_CU_VARIANT_BITSLICE_ALU).
+// OPT (T3_OPT_* bitmask) selects which small pieces of work move from the
+// saturated ALU pipe to the FMA pipe; T3_OPT_DEFAULT is the measured best.
 // Each warp owns an 8 KiB shared-memory slot and an mbarrier.  While the
 // warp runs the 48 rounds of tile t, the TMA engine (cp.async.bulk, SASS
 // UBLKCP) streams tile t+1 from HBM into the slot, so the warps' load phases
@@ -111,7 +113,7 @@ __device__ __forceinline__ void t3_mbar_wait(uint32_t bar, uint32_t parity) {
         : "memory");
 }
 
-template <bool FMA>
+template <int OPT>
 __global__ void __launch_bounds__(T3_BS_THREADS, T3_BS_MIN_CTAS)
 t3_bs_tma_kernel(const uint8_t* in, uint8_t* out, uint64_t ntiles, const __grid_constant__ T3BsTable tab) {
     __shared__ __align__(128) uint4 slot[T3_BS_THREADS / 32][T3_TILE_BLOCKS / 2];
@@ -148,7 +150,7 @@ t3_bs_tma_kernel(const uint8_t* in, uint8_t* out, uint64_t ntiles, const __grid_
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             t3_tma_fetch(sdst, in + next * (T3_TILE_BLOCKS * 8), T3_TILE_BLOCKS * 8, sbar);
         }
-        t3_tile32<FMA>(lo, hi, tab.w);
+        t3_tile32<OPT>(lo, hi, tab.w);
         uint4* dst = reinterpret_cast<uint4*>(out + tile * (T3_TILE_BLOCKS * 8)) + lane;
 #pragma unroll
         for (int j = 0; j < 16; ++j)

@@ -47,13 +47,19 @@ T3_FI uint32_t prmt(uint32_t a, uint32_t b) {
 #endif
 }
 
-// x ^ d for a key-correction word d in {0, ~0}.  FMA = true computes it as
+// Code-generation options of the bitsliced core (template bitmask OPT).
+enum : int {
+    T3_OPT_DFMA = 1,    // E-duplicate key corrections as IMAD (FMA pipe)
+    T3_OPT_SHRFMA = 2,  // transpose right shifts as IMAD.HI (FMA pipe)
+};
+
+// x ^ d for a key-correction word d in {0, ~0}.  OPT & DFMA computes it as
 // x * s + d with s = d | 1 (= +1 or -1): an IMAD on the FMA pipe, which is
 // otherwise idle, instead of a LOP3 on the saturated ALU pipe.
-template <bool FMA>
+template <int OPT>
 T3_FI uint32_t t3_dfix(uint32_t x, uint32_t d, uint32_t s) {
 #ifdef __CUDA_ARCH__
-    if (FMA) {
+    if (OPT & T3_OPT_DFMA) {
         uint32_t r;
         asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(x), "r"(s), "r"(d));
         return r;
@@ -63,11 +69,11 @@ T3_FI uint32_t t3_dfix(uint32_t x, uint32_t d, uint32_t s) {
     return x ^ d;
 }
 
-// a >> S; FMA = true uses IMAD.HI (a * 2^(32-S) >> 32) on the FMA pipe.
-template <int S, bool FMA>
+// a >> S; OPT & SHRFMA uses IMAD.HI (a * 2^(32-S) >> 32) on the FMA pipe.
+template <int S, int OPT>
 T3_FI uint32_t t3_shr(uint32_t a) {
 #ifdef __CUDA_ARCH__
-    if (FMA) {
+    if (OPT & T3_OPT_SHRFMA) {
         uint32_t r;
         asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(1u << (32 - S)));
         return r;
@@ -98,7 +104,7 @@ struct T3BsTable {
 // In-register transpose of a 32x32 bit matrix: afterwards x[k] bit m is the
 // old x[m] bit k.  Stages 16 and 8 are byte moves (PRMT); stages 4, 2, 1
 // are mask-select swaps (two shifts + two lop3 per pair).
-template <bool FMA>
+template <int OPT>
 T3_FI void t3_transpose32(uint32_t (&x)[32]) {
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
@@ -118,20 +124,20 @@ T3_FI void t3_transpose32(uint32_t (&x)[32]) {
         if (r & 4) continue;
         const uint32_t a = x[r], b = x[r + 4];
         x[r] = lop3<0xE4>(a, b << 4, 0x0F0F0F0Fu);  // 0xE4: c ? a : b
-        x[r + 4] = lop3<0xE4>(t3_shr<4, FMA>(a), b, 0x0F0F0F0Fu);
+        x[r + 4] = lop3<0xE4>(t3_shr<4, OPT>(a), b, 0x0F0F0F0Fu);
     }
 #pragma unroll
     for (int r = 0; r < 32; ++r) {
         if (r & 2) continue;
         const uint32_t a = x[r], b = x[r + 2];
         x[r] = lop3<0xE4>(a, b << 2, 0x33333333u);
-        x[r + 2] = lop3<0xE4>(t3_shr<2, FMA>(a), b, 0x33333333u);
+        x[r + 2] = lop3<0xE4>(t3_shr<2, OPT>(a), b, 0x33333333u);
     }
 #pragma unroll
     for (int r = 0; r < 32; r += 2) {
         const uint32_t a = x[r], b = x[r + 1];
         x[r] = lop3<0xE4>(a, b << 1, 0x55555555u);
-        x[r + 1] = lop3<0xE4>(t3_shr<1, FMA>(a), b, 0x55555555u);
+        x[r + 1] = lop3<0xE4>(t3_shr<1, OPT>(a), b, 0x55555555u);
     }
 }
 
@@ -144,26 +150,26 @@ T3_FI void t3_xor_table(uint32_t (&h)[32], const KP k) {
 // All 48 rounds (3 passes of 16) on halves A (initial L) and B (initial R).
 // The pass-final half swaps of the reference (tdes.cpp:151-159) are role
 // renamings: pass 2 runs with the roles of A and B exchanged.
-template <bool FMA, class KP>
+template <int OPT, class KP>
 T3_FI void t3_cipher(uint32_t (&A)[32], uint32_t (&B)[32], const KP w) {
     t3_xor_table(A, w + T3_TAB_PRE);
     t3_xor_table(B, w + T3_TAB_PRE + 32);
 #pragma unroll 1
     for (int it = 0; it < 8; ++it) {
-        t3_round<FMA>(A, B, w + T3_TAB_ROUND + (2 * it) * T3_ROUND_WORDS);
-        t3_round<FMA>(B, A, w + T3_TAB_ROUND + (2 * it + 1) * T3_ROUND_WORDS);
+        t3_round<OPT>(A, B, w + T3_TAB_ROUND + (2 * it) * T3_ROUND_WORDS);
+        t3_round<OPT>(B, A, w + T3_TAB_ROUND + (2 * it + 1) * T3_ROUND_WORDS);
     }
     t3_xor_table(A, w + T3_TAB_RW1);
 #pragma unroll 1
     for (int it = 0; it < 8; ++it) {
-        t3_round<FMA>(B, A, w + T3_TAB_ROUND + (16 + 2 * it) * T3_ROUND_WORDS);
-        t3_round<FMA>(A, B, w + T3_TAB_ROUND + (17 + 2 * it) * T3_ROUND_WORDS);
+        t3_round<OPT>(B, A, w + T3_TAB_ROUND + (16 + 2 * it) * T3_ROUND_WORDS);
+        t3_round<OPT>(A, B, w + T3_TAB_ROUND + (17 + 2 * it) * T3_ROUND_WORDS);
     }
     t3_xor_table(B, w + T3_TAB_RW2);
 #pragma unroll 1
     for (int it = 0; it < 8; ++it) {
-        t3_round<FMA>(A, B, w + T3_TAB_ROUND + (32 + 2 * it) * T3_ROUND_WORDS);
-        t3_round<FMA>(B, A, w + T3_TAB_ROUND + (33 + 2 * it) * T3_ROUND_WORDS);
+        t3_round<OPT>(A, B, w + T3_TAB_ROUND + (32 + 2 * it) * T3_ROUND_WORDS);
+        t3_round<OPT>(B, A, w + T3_TAB_ROUND + (33 + 2 * it) * T3_ROUND_WORDS);
     }
     t3_xor_table(A, w + T3_TAB_POST);
     t3_xor_table(B, w + T3_TAB_POST + 32);
@@ -171,13 +177,13 @@ T3_FI void t3_cipher(uint32_t (&A)[32], uint32_t (&B)[32], const KP w) {
 
 // One thread's 32 blocks: lo[m]/hi[m] are the little-endian words holding
 // bytes 0..3 / 4..7 of block m.  Transforms in place.
-template <bool FMA, class KP>
+template <int OPT, class KP>
 T3_FI void t3_tile32(uint32_t (&lo)[32], uint32_t (&hi)[32], const KP w) {
-    t3_transpose32<FMA>(lo);
-    t3_transpose32<FMA>(hi);
+    t3_transpose32<OPT>(lo);
+    t3_transpose32<OPT>(hi);
     uint32_t A[32] = T3_GATHER_A(lo, hi);
     uint32_t B[32] = T3_GATHER_B(lo, hi);
-    t3_cipher<FMA>(A, B, w);
+    t3_cipher<OPT>(A, B, w);
     {
         uint32_t olo[32] = T3_SCATTER_LO(A, B);
         uint32_t ohi[32] = T3_SCATTER_HI(A, B);
@@ -187,6 +193,6 @@ T3_FI void t3_tile32(uint32_t (&lo)[32], uint32_t (&hi)[32], const KP w) {
             hi[k] = ohi[k];
         }
     }
-    t3_transpose32<FMA>(lo);
-    t3_transpose32<FMA>(hi);
+    t3_transpose32<OPT>(lo);
+    t3_transpose32<OPT>(hi);
 }

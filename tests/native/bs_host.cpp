@@ -20,7 +20,7 @@ extern "C" int bs_host_ecb(const std::uint8_t* in, std::uint8_t* out, std::size_
             std::memcpy(&lo[m], in + 8 * (base + m), 4);
             std::memcpy(&hi[m], in + 8 * (base + m) + 4, 4);
         }
-        t3_tile32<false>(lo, hi, static_cast<const std::uint32_t*>(tab.w));
+        t3_tile32<0>(lo, hi, static_cast<const std::uint32_t*>(tab.w));
         for (int m = 0; m < 32; ++m) {
             std::memcpy(out + 8 * (base + m), &lo[m], 4);
             std::memcpy(out + 8 * (base + m) + 4, &hi[m], 4);
