@@ -103,12 +103,16 @@ int t3des_cu_ecb_device(t3des_cu_ctx* ctx, int direction, const void* din, void*
                         size_t len, void* stream);
 
 /* Host buffers, end to end: chunked H2D -> kernel -> D2H pipelined over
- * three streams; returns when `out` holds the result.  This is the entry
+ * several streams (t3des_cu_set_pipeline); returns when `out` holds the result.  This is the entry
  * a Backend::Cuda branch of run_batch calls (same contract as
  * encrypt_batch/decrypt_batch).  Pinned buffers (t3des_cu_host_alloc)
  * give full PCIe overlap; pageable buffers work, more slowly. */
 int t3des_cu_ecb_host(t3des_cu_ctx* ctx, int direction, const uint8_t* in, uint8_t* out,
                       size_t len);
+
+/* Host-path pipeline shape: bytes per stage (multiple of 8; default 32 MiB)
+ * and number of streams/staging buffers (1..8; default 3). */
+int t3des_cu_set_pipeline(t3des_cu_ctx* ctx, size_t chunk_bytes, int streams);
 
 /* Host buffers sharded by contiguous block ranges (multiples of 1024
  * blocks) over `ndev` devices, one host thread and context per device; no

@@ -50,6 +50,7 @@ SIGNATURES = {
     "t3des_cu_set_launch": (_i, [_vp, _sz, _i]),
     "t3des_cu_ecb_device": (_i, [_vp, _i, _vp, _vp, _sz, _vp]),
     "t3des_cu_ecb_host": (_i, [_vp, _i, _vp, _vp, _sz]),
+    "t3des_cu_set_pipeline": (_i, [_vp, _sz, _i]),
     "t3des_cu_ecb_multi": (_i, [ctypes.POINTER(_i), _i, _u64p, _i, _vp, _vp, _sz]),
     "t3des_cu_shard_range": (_i, [ctypes.c_uint64, _i, _i, _u64p, _u64p]),
     "t3des_cu_host_alloc": (_i, [_sz, ctypes.POINTER(_vp)]),

@@ -193,6 +193,9 @@ class Engine:
     def set_launch(self, chunk_blocks: int = 0, work_group: int = 0) -> None:
         _raise(self._lib.t3des_cu_set_launch(self._h, int(chunk_blocks), int(work_group)))
 
+    def set_pipeline(self, chunk_bytes: int = 32 << 20, streams: int = 3) -> None:
+        _raise(self._lib.t3des_cu_set_pipeline(self._h, int(chunk_bytes), int(streams)))
+
     def ecb_device(self, direction: int, din: int, dout: int, nbytes: int, stream: int = 0) -> None:
         _raise(self._lib.t3des_cu_ecb_device(self._h, int(direction), din, dout, int(nbytes), stream or None))
 

@@ -30,15 +30,17 @@ struct t3des_cu_ctx {
     T3SpKeyParam sp[2];
     std::uint32_t* d_sp = nullptr;  // 8x64 fused S/P table (2 KiB)
     unsigned long long* d_acc = nullptr;
-    cudaStream_t st[3] = {nullptr, nullptr, nullptr};
-    std::uint8_t* buf[3] = {nullptr, nullptr, nullptr};
+    static constexpr int kMaxStreams = 8;
+    cudaStream_t st[kMaxStreams] = {};
+    std::uint8_t* buf[kMaxStreams] = {};
     std::size_t buf_bytes = 0;
+    std::size_t pipe_chunk = std::size_t(32) << 20;  // bytes per pipeline stage
+    int pipe_streams = 3;
     std::uint64_t launches = 0;
 };
 
 namespace {
 
-constexpr std::size_t kHostChunkBytes = std::size_t(64) << 20;  // per pipeline stage
 constexpr int kSpSmemBytes = 8 * 64 * 32 * 4;                   // 64 KiB
 
 // Restores the caller's current device on scope exit.
@@ -305,27 +307,39 @@ int t3des_cu_ecb_host(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uin
     if (rc) return rc;
     if (!len) return T3DES_CU_OK;
     DeviceScope scope(c->device);
-    const std::size_t chunk = std::min(len, kHostChunkBytes);
-    if (c->buf_bytes < chunk) {
+    const std::size_t chunk = std::min(len, c->pipe_chunk);
+    const int ns = c->pipe_streams;
+    if (c->buf_bytes < chunk || !c->buf[ns - 1]) {
         for (auto& b : c->buf) {
             if (b) cudaFree(b);
             b = nullptr;
         }
         c->buf_bytes = 0;
-        for (auto& b : c->buf) T3_CK(cudaMalloc(&b, chunk));
+        for (int i = 0; i < ns; ++i) T3_CK(cudaMalloc(&c->buf[i], chunk));
         c->buf_bytes = chunk;
     }
+    // Stage k: H2D, kernel, D2H on stream k % ns (in-order per stream, so a
+    // stream's buffer is free again when its next stage starts); stages on
+    // different streams overlap copies in both directions with kernels.
     std::size_t k = 0;
     for (std::size_t off = 0; off < len; off += chunk, ++k) {
         const std::size_t n = std::min(chunk, len - off);
-        cudaStream_t s = c->st[k % 3];
-        std::uint8_t* b = c->buf[k % 3];
+        cudaStream_t s = c->st[k % ns];
+        std::uint8_t* b = c->buf[k % ns];
         T3_CK(cudaMemcpyAsync(b, in + off, n, cudaMemcpyHostToDevice, s));
         rc = run_device(c, dir, b, b, n / 8, s);
         if (rc) return rc;
         T3_CK(cudaMemcpyAsync(out + off, b, n, cudaMemcpyDeviceToHost, s));
     }
-    for (auto& s : c->st) T3_CK(cudaStreamSynchronize(s));
+    for (int i = 0; i < ns; ++i) T3_CK(cudaStreamSynchronize(c->st[i]));
+    return T3DES_CU_OK;
+}
+
+int t3des_cu_set_pipeline(t3des_cu_ctx* c, std::size_t chunk_bytes, int streams) {
+    if (!c || streams < 1 || streams > t3des_cu_ctx::kMaxStreams || chunk_bytes < 8 || chunk_bytes % 8)
+        return T3DES_CU_ERR_ARG;
+    c->pipe_chunk = chunk_bytes;
+    c->pipe_streams = streams;
     return T3DES_CU_OK;
 }
 

@@ -280,6 +280,79 @@ static int build(circ_t* st, tt_t T, tt_t M, int avail, int depth) {
     return best_g;
 }
 
+/* ---- resubstitution post-pass -------------------------------------------
+ * For each gate h, try to recompute tt[h] (or ~tt[h]: consumers absorb an
+ * inversion) as one LUT3 of three signals earlier in topological order.  If
+ * the rewrite leaves some gate without fanout, drop the dead gates.  Repeat
+ * until no rewrite helps. */
+static int fanouts(const circ_t* c, const int* outs, int* fo) {
+    memset(fo, 0, sizeof(int) * MAXG);
+    for (int g = 6; g < c->n; g++)
+        for (int k = 0; k < 3; k++) fo[c->in[g][k]]++;
+    for (int o = 0; o < 4; o++) fo[outs[o]]++;
+    return 0;
+}
+
+/* remove gates with zero fanout (not outputs), compacting indices */
+static void sweep(circ_t* c, int* outs) {
+    for (;;) {
+        int fo[MAXG];
+        fanouts(c, outs, fo);
+        int dead = -1;
+        for (int g = c->n - 1; g >= 6; g--)
+            if (fo[g] == 0) { dead = g; break; }
+        if (dead < 0) return;
+        for (int g = dead; g < c->n - 1; g++) {
+            c->tt[g] = c->tt[g + 1];
+            c->lut[g] = c->lut[g + 1];
+            for (int k = 0; k < 3; k++) c->in[g][k] = c->in[g + 1][k];
+        }
+        c->n--;
+        for (int g = 6; g < c->n; g++)
+            for (int k = 0; k < 3; k++)
+                if (c->in[g][k] > dead) c->in[g][k]--;
+        for (int o = 0; o < 4; o++)
+            if (outs[o] > dead) outs[o]--;
+    }
+}
+
+/* only-used-by: does removing h's current inputs' single use free gates? */
+static int freed_if_rewired(const circ_t* c, const int* fo, int h, int a, int b, int cc) {
+    int freed = 0;
+    for (int k = 0; k < 3; k++) {
+        int x = c->in[h][k];
+        if (x < 6) continue;
+        int uses_new = (x == a) + (x == b) + (x == cc);
+        int uses_old = (c->in[h][0] == x) + (c->in[h][1] == x) + (c->in[h][2] == x);
+        if (fo[x] - uses_old + uses_new == 0) freed++;
+    }
+    return freed;
+}
+
+static void resub(circ_t* c, int* outs, const tt_t* tgt) {
+    int improved = 1;
+    while (improved) {
+        improved = 0;
+        int fo[MAXG];
+        fanouts(c, outs, fo);
+        for (int h = c->n - 1; h >= 6 && !improved; h--) {
+            for (int a = 0; a < h && !improved; a++)
+                for (int b = a + 1; b < h && !improved; b++)
+                    for (int cc = b + 1; cc < h && !improved; cc++) {
+                        if (!freed_if_rewired(c, fo, h, a, b, cc)) continue;
+                        uint8_t l;
+                        tt_t T = c->tt[h];
+                        if (find_lut3(c->tt[a], c->tt[b], c->tt[cc], T, ~0ull, &l)) {
+                            c->in[h][0] = a; c->in[h][1] = b; c->in[h][2] = cc; c->lut[h] = l;
+                            sweep(c, outs);
+                            improved = 1;
+                        }
+                    }
+        }
+    }
+    (void)tgt;
+}
+
 static tt_t out_tt(int box, int bit) {
     tt_t t = 0;
     for (int p = 0; p < 64; p++) {
@@ -345,6 +418,7 @@ int main(int argc, char** argv) {
             outs[ord[k]] = g;
         }
         if (!ok) continue;
+        resub(&c, outs, tgt);
         if (c.n < best.n) {
             best = c;
             memcpy(best_out, outs, sizeof outs);
