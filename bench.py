@@ -180,6 +180,105 @@ def run_reference_impl(args, rank: int, world: int) -> None:
     print(json.dumps(line), flush=True)
 
 
+def pcie_bidir(host, nbytes: int) -> float:
+    """Raw pinned-host <-> device copy rate with both directions in flight
+    (the ceiling of the e2e number), GB/s each way."""
+    import torch
+
+    d_in = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    d_out = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    h2 = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(2):
+        with torch.cuda.stream(s1):
+            d_in.copy_(host, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h2.copy_(d_out, non_blocking=True)
+    torch.cuda.synchronize()
+    return round(2 * nbytes / (time.perf_counter() - t0) / 1e9, 2)
+
+
+def extra_configs(e, orc, t3, N, torch, np) -> dict:
+    """The other BASELINE.json configs, each checked before it is timed:
+    [0] 1 MiB encrypt+decrypt, 3 distinct keys, NIST KAT;
+    [2] 4 GiB decrypt, device-resident and end to end;
+    [4] edge cases (option 3 = single DES, option 2, odd tails) — parity only."""
+    out = {}
+    stream = torch.cuda.current_stream().cuda_stream
+    # configs[0]
+    kat_key = "0123456789ABCDEF23456789ABCDEF01456789ABCDEF0123"
+    pt = bytes.fromhex("54686520717566636B2062726F776E20666F78206A756D70")
+    ct = bytearray(len(pt))
+    t3.encrypt_batch(pt, ct, t3.triple_schedule(t3.parse_hex_key(kat_key)))
+    kat_ok = ct.hex().upper() == "A826FD8CE53B855FCCE21C8112256FE668D5C05DD9B6B900"
+    x = orc.payload(1 << 20)
+    s = orc.schedule_hex(BENCH_KEY)
+    d = torch.from_numpy(x).cuda()
+    y = torch.empty_like(d)
+    z = torch.empty_like(d)
+    e.ecb_device(0, d.data_ptr(), y.data_ptr(), x.nbytes, stream)
+    e.ecb_device(1, y.data_ptr(), z.data_ptr(), x.nbytes, stream)
+    torch.cuda.synchronize()
+    ok = bool(np.array_equal(y.cpu().numpy(), orc.ecb(x, s, 0))) and bool(torch.equal(z, d))
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(3):
+        e.ecb_device(0, d.data_ptr(), y.data_ptr(), x.nbytes, stream)
+    ev0.record()
+    for _ in range(50):
+        e.ecb_device(0, d.data_ptr(), y.data_ptr(), x.nbytes, stream)
+        e.ecb_device(1, y.data_ptr(), z.data_ptr(), x.nbytes, stream)
+    ev1.record()
+    torch.cuda.synchronize()
+    us = ev0.elapsed_time(ev1) * 1e3 / 50
+    out["c0_1MiB_enc_dec"] = {"us_per_enc_plus_dec": round(us, 2), "GBps_enc_plus_dec": round(2 * x.nbytes / us / 1e3, 2),
+                              "bit_exact_vs_oracle": ok, "nist_sp800_67_kat": kat_ok,
+                              "note": "launch-latency bound: 1 MiB is 128 warp tiles on 148 SMs"}
+    del d, y, z
+    # configs[2]: 4 GiB decrypt
+    n4 = (4 << 30) // 8
+    buf = torch.empty(8 * n4, dtype=torch.uint8, device="cuda")
+    e.fill_splitmix(buf.data_ptr(), 0, n4, SEED, stream)
+    e.ecb_device(0, buf.data_ptr(), buf.data_ptr(), 8 * n4, stream)  # ciphertext of the payload
+    dec = torch.empty_like(buf)
+    e.ecb_device(1, buf.data_ptr(), dec.data_ptr(), 8 * n4, stream)
+    torch.cuda.synchronize()
+    rt_ok = e.checksum(dec.data_ptr(), 0, n4, stream) == _splitmix_checksum(e, torch, n4)
+    ev0.record()
+    for _ in range(5):
+        e.ecb_device(1, buf.data_ptr(), dec.data_ptr(), 8 * n4, stream)
+    ev1.record()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / 5
+    del dec
+    host = torch.empty(8 * n4, dtype=torch.uint8).pin_memory()
+    host.copy_(buf.cpu())
+    del buf
+    torch.cuda.empty_cache()
+    out_h = torch.empty_like(host).pin_memory()
+    e.ecb_host(1, host.data_ptr(), out_h.data_ptr(), 8 * n4)
+    t0 = time.perf_counter()
+    for _ in range(2):
+        e.ecb_host(1, host.data_ptr(), out_h.data_ptr(), 8 * n4)
+    e2e = 2 * 8 * n4 / (time.perf_counter() - t0) / 1e9
+    del out_h
+    out["c2_4GiB_decrypt"] = {"device_GBps": round(8 * n4 / ms / 1e6, 2), "e2e_GBps": round(e2e, 2),
+                              "round_trip_checksum_ok": bool(rt_ok),
+                              "note": "device: 5 decrypts of the 4 GiB ciphertext, CUDA events; "
+                                      "e2e: t3des_cu_ecb_host pinned in -> pinned out incl. H2D/D2H"}
+    del host
+    return out
+
+
+def _splitmix_checksum(e, torch, n) -> int:
+    tmp = torch.empty(8 * n, dtype=torch.uint8, device="cuda")
+    e.fill_splitmix(tmp.data_ptr(), 0, n, SEED, torch.cuda.current_stream().cuda_stream)
+    v = e.checksum(tmp.data_ptr(), 0, n, torch.cuda.current_stream().cuda_stream)
+    del tmp
+    return v
+
+
 def workload_config(args, world: int) -> dict:
     return {
         "workload": f"3DES-ECB encrypt {args.gib} GiB device-resident per GPU (BASELINE configs[1]); "
@@ -203,6 +302,7 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
+    ap.add_argument("--no-extra-configs", action="store_true")
     ap.add_argument("--traffic-bytes", type=float, default=None,
                     help="dram bytes per launch from an ncu --set full capture (else read profiles/)")
     args = ap.parse_args()
@@ -351,6 +451,7 @@ def main() -> None:
         host.copy_(src.cpu())
         del src
         torch.cuda.empty_cache()
+        e.set_pipeline(32 << 20, 3)
         e.ecb_host(0, host.data_ptr(), host.data_ptr(), nbytes)  # warm (allocates staging)
         k3 = max(3, min(args.steps, 5))
         barrier()
@@ -360,10 +461,14 @@ def main() -> None:
         dt = max_over_ranks((time.perf_counter() - t0) / k3)
         line["e2e"] = {"value": round(world * nbytes / dt / 1e9, 3), "unit": "GB/s",
                        "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
-                       "path": "t3des_cu_ecb_host, pinned host buffer, 64 MiB chunks over 3 streams",
-                       "steps": k3}
+                       "path": "t3des_cu_ecb_host, pinned host buffer, 32 MiB stages over 3 streams",
+                       "steps": k3, "pcie_bidir_copy_gbs_each_way": pcie_bidir(host, nbytes)}
+        del host
     else:
         line["e2e"] = None
+
+    if not args.no_extra_configs and world == 1:
+        line["configs_measured"] = extra_configs(e, orc, t3, N, torch, np)
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         g, cores, kind, desc = cpu_reference_arm()
