@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -225,6 +226,12 @@ int t3des_cu_create(int device, t3des_cu_ctx** out) {
             break;
         }
         c->bs_occ = std::max(std::min(c->bs_occ, occ_ldg), 1);
+        // Tuning override (experiments only): resident CTAs per SM for the
+        // persistent bitsliced grid.
+        if (const char* e = std::getenv("T3DES_BS_CTAS_PER_SM")) {
+            const int v = std::atoi(e);
+            if (v > 0) c->bs_occ = v;
+        }
         c->sp_occ = std::max(c->sp_occ, 1);
         std::uint32_t sp[8][64];
         t3b::build_sp_tables(sp);
