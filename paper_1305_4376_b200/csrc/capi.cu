@@ -96,7 +96,7 @@ int launch_bitslice(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8
                                                                        : T3_OPT_SHRFMA;
         if (tma && opt == 0)
             t3_bs_tma_kernel<0><<<unsigned(grid), threads, 0, s>>>(in, out, full, c->bs[dir]);
-        else if (tma && opt == T3_OPT_DFMA)
+        else if (tma && (opt & T3_OPT_DFMA))
             t3_bs_tma_kernel<T3_OPT_DFMA><<<unsigned(grid), threads, 0, s>>>(in, out, full, c->bs[dir]);
         else if (tma)
             t3_bs_tma_kernel<T3_OPT_SHRFMA><<<unsigned(grid), threads, 0, s>>>(in, out, full, c->bs[dir]);
