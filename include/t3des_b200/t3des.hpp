@@ -11,6 +11,8 @@
 //   dispatch.hpp:39-42  plan_dispatch, ChunkSpan     same
 //   dispatch.hpp:64-69  encrypt_batch/decrypt_batch  same signatures
 //   dispatch.hpp:44-47, tdes.hpp:25-28  InputLengthError, KeyFormatError
+//   dispatch.hpp:32,49-91  PaddingMode, PaddingError, IoError, StreamReport,
+//                      encrypt_stream/decrypt_stream, pkcs7_pad/pkcs7_unpad
 //
 // Backend::Cuda sends the whole batch through the C ABI (t3des_cu.h) in
 // one call; there is no CPU cipher in this library (ScalarReference and
@@ -20,6 +22,7 @@
 #include <array>
 #include <cstddef>
 #include <cstdint>
+#include <iosfwd>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -50,6 +53,17 @@ class KeyFormatError : public std::runtime_error {
 class InputLengthError : public std::runtime_error {
   public:
     using std::runtime_error::runtime_error;
+};
+
+class PaddingError : public std::runtime_error {
+  public:
+    using std::runtime_error::runtime_error;
+};
+
+class IoError : public std::runtime_error {
+  public:
+    IoError(const std::string& what, std::uint64_t offset) : std::runtime_error(what), byte_offset(offset) {}
+    std::uint64_t byte_offset;
 };
 
 // CUDA runtime / device failures (no device is an error, never a fallback).
@@ -100,5 +114,27 @@ void encrypt_batch(std::span<const std::uint8_t> in, std::span<std::uint8_t> out
                    const TripleSchedule& ts, const DispatchConfig& cfg);
 void decrypt_batch(std::span<const std::uint8_t> in, std::span<std::uint8_t> out,
                    const TripleSchedule& ts, const DispatchConfig& cfg);
+
+enum class PaddingMode { None, Pkcs7 };
+
+struct StreamReport {
+    std::uint64_t bytes_in = 0;
+    std::uint64_t bytes_out = 0;
+    std::uint64_t chunks = 0;
+    double compute_seconds = 0.0;  // engine time not overlapped with I/O
+    double io_seconds = 0.0;       // reads and writes
+};
+
+// Chunked streams (chunk = cfg.chunk_blocks blocks), Backend::Cuda only:
+// chunk k+1 is read while chunk k runs on the GPU.  Same bytes, padding and
+// errors as the reference's encrypt_stream/decrypt_stream.
+StreamReport encrypt_stream(std::istream& source, std::ostream& sink, const TripleSchedule& ts,
+                            const DispatchConfig& cfg, PaddingMode pad);
+StreamReport decrypt_stream(std::istream& source, std::ostream& sink, const TripleSchedule& ts,
+                            const DispatchConfig& cfg, PaddingMode pad);
+
+// PKCS#7 over 8-byte blocks: always appends 1..8 bytes; unpad throws PaddingError.
+void pkcs7_pad(std::vector<std::uint8_t>& data);
+void pkcs7_unpad(std::vector<std::uint8_t>& data);
 
 }  // namespace t3des

@@ -32,7 +32,8 @@ extern "C" {
 #endif
 
 /* Status codes.  The C++ layer maps 1-2 to InputLengthError
- * (dispatch.hpp:44-47) and 3 to KeyFormatError (tdes.hpp:25-28). */
+ * (dispatch.hpp:44-47), 3 to KeyFormatError (tdes.hpp:25-28), 8 to
+ * PaddingError and 9 to IoError (dispatch.hpp:49-59). */
 #define T3DES_CU_OK 0
 #define T3DES_CU_ERR_LENGTH 1      /* byte length not a multiple of 8       */
 #define T3DES_CU_ERR_OVERLAP 2     /* in/out partially overlap              */
@@ -41,6 +42,8 @@ extern "C" {
 #define T3DES_CU_ERR_NO_DEVICE 5   /* no CUDA device / not sm_100           */
 #define T3DES_CU_ERR_CUDA 6        /* a CUDA runtime call failed            */
 #define T3DES_CU_ERR_NO_SCHEDULE 7 /* t3des_cu_set_schedule not called yet  */
+#define T3DES_CU_ERR_PADDING 8     /* malformed PKCS#7 padding (PaddingError) */
+#define T3DES_CU_ERR_IO 9          /* stream read/write failure (IoError)    */
 
 #define T3DES_CU_ENCRYPT 0
 #define T3DES_CU_DECRYPT 1
@@ -125,6 +128,30 @@ int t3des_cu_ecb_multi(const int* devices, int ndev, const uint64_t sub48[48], i
  * bench.py's torchrun ranks): [first, first + count), boundaries at
  * floor(g*N/ndev) rounded down to 1024-block tiles; the last shard ends at N. */
 int t3des_cu_shard_range(uint64_t nblocks, int ndev, int g, uint64_t* first, uint64_t* count);
+
+/* ---- streams ------------------------------------------------------------- */
+
+/* Mirrors the reference's StreamReport (dispatch.hpp:71-77). */
+typedef struct t3des_cu_stream_report {
+    uint64_t bytes_in;
+    uint64_t bytes_out;
+    uint64_t chunks;
+    double compute_seconds; /* engine time not overlapped with I/O */
+    double io_seconds;      /* reads and writes                    */
+    uint64_t error_offset;  /* byte offset of an IO error          */
+} t3des_cu_stream_report;
+
+/* Replaces encrypt_stream/decrypt_stream (dispatch.hpp:79-91,
+ * dispatch.cpp:111-206) on file descriptors: reads chunk_blocks*8-byte
+ * chunks from in_fd, writes the transformed bytes to out_fd in order.
+ * pkcs7 = 1: encrypt pads the last chunk, decrypt strips and checks the
+ * padding of the last chunk (T3DES_CU_ERR_PADDING).  Without padding the
+ * input length must be a multiple of 8 (T3DES_CU_ERR_LENGTH).  Read/write
+ * failures return T3DES_CU_ERR_IO with report->error_offset set.  Chunk k+1
+ * is read while chunk k runs on the device; output equals the reference's
+ * byte for byte. */
+int t3des_cu_stream_fd(t3des_cu_ctx* ctx, int direction, int in_fd, int out_fd, size_t chunk_blocks,
+                       int pkcs7, t3des_cu_stream_report* report);
 
 /* ---- utilities --------------------------------------------------------- */
 

@@ -23,16 +23,24 @@ from .api import (  # noqa: F401
     DispatchConfig,
     Engine,
     InputLengthError,
+    IoError,
     KeyFormatError,
     KeyingOption,
+    PaddingError,
+    PaddingMode,
+    StreamReport,
     TripleKey,
     TripleSchedule,
     decrypt_batch,
+    decrypt_stream,
     encrypt_batch,
+    encrypt_stream,
     engine,
     key_schedule,
     load_block,
     parse_hex_key,
+    pkcs7_pad,
+    pkcs7_unpad,
     plan_dispatch,
     store_block,
     to_hex,

@@ -22,6 +22,8 @@ ERR_ARG = 4
 ERR_NO_DEVICE = 5
 ERR_CUDA = 6
 ERR_NO_SCHEDULE = 7
+ERR_PADDING = 8
+ERR_IO = 9
 
 ENCRYPT = 0
 DECRYPT = 1
@@ -31,6 +33,14 @@ VARIANT_BITSLICE_LDG = 2
 VARIANT_BITSLICE_ALU = 3
 VARIANT_BITSLICE_DFMA = 4
 VARIANT_BITSLICE_SHRFMA = 5
+
+class StreamReportC(ctypes.Structure):
+    """t3des_cu_stream_report (include/t3des_cu.h)."""
+
+    _fields_ = [("bytes_in", ctypes.c_uint64), ("bytes_out", ctypes.c_uint64), ("chunks", ctypes.c_uint64),
+                ("compute_seconds", ctypes.c_double), ("io_seconds", ctypes.c_double),
+                ("error_offset", ctypes.c_uint64)]
+
 
 # Every symbol include/t3des_cu.h declares: name -> (restype, argtypes).
 _u64p = ctypes.POINTER(ctypes.c_uint64)
@@ -51,6 +61,7 @@ SIGNATURES = {
     "t3des_cu_ecb_device": (_i, [_vp, _i, _vp, _vp, _sz, _vp]),
     "t3des_cu_ecb_host": (_i, [_vp, _i, _vp, _vp, _sz]),
     "t3des_cu_set_pipeline": (_i, [_vp, _sz, _i]),
+    "t3des_cu_stream_fd": (_i, [_vp, _i, _i, _i, _sz, _i, ctypes.POINTER(StreamReportC)]),
     "t3des_cu_ecb_multi": (_i, [ctypes.POINTER(_i), _i, _u64p, _i, _vp, _vp, _sz]),
     "t3des_cu_shard_range": (_i, [ctypes.c_uint64, _i, _i, _u64p, _u64p]),
     "t3des_cu_host_alloc": (_i, [_sz, ctypes.POINTER(_vp)]),

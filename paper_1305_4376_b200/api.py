@@ -36,6 +36,18 @@ class InputLengthError(ValueError):
     (dispatch.hpp:44-47)."""
 
 
+class PaddingError(ValueError):
+    """Malformed PKCS#7 padding (dispatch.hpp:49-52)."""
+
+
+class IoError(OSError):
+    """Stream read/write failure at byte_offset (dispatch.hpp:54-59)."""
+
+    def __init__(self, msg: str, byte_offset: int):
+        super().__init__(msg)
+        self.byte_offset = byte_offset
+
+
 class CudaError(RuntimeError):
     """Device or CUDA runtime failure; never silently falls back to a CPU."""
 
@@ -52,6 +64,8 @@ def _raise(rc: int, what: str = "") -> None:
         raise InputLengthError(msg)
     if rc == N.ERR_KEY:
         raise KeyFormatError(msg)
+    if rc == N.ERR_PADDING:
+        raise PaddingError(msg)
     if rc == N.ERR_ARG:
         raise ValueError(msg)
     raise CudaError(msg, rc)
@@ -311,3 +325,134 @@ def encrypt_batch(src, dst, ts: TripleSchedule, cfg: DispatchConfig | None = Non
 
 def decrypt_batch(src, dst, ts: TripleSchedule, cfg: DispatchConfig | None = None) -> None:
     _run_batch(src, dst, ts, cfg or DispatchConfig(), N.DECRYPT)
+
+
+# ---- streams (dispatch.hpp:32,71-91) ----------------------
+
+class PaddingMode(enum.Enum):
+    NONE = 0
+    PKCS7 = 1
+
+
+@dataclass(frozen=True)
+class StreamReport:
+    bytes_in: int
+    bytes_out: int
+    chunks: int
+    compute_seconds: float
+    io_seconds: float
+
+
+def pkcs7_pad(data: bytes | bytearray) -> bytes:
+    pad = 8 - len(data) % 8
+    return bytes(data) + bytes([pad]) * pad
+
+
+def pkcs7_unpad(data: bytes | bytearray) -> bytes:
+    if not data or len(data) % 8:
+        raise PaddingError("PKCS#7 data length must be a positive multiple of 8")
+    pad = data[-1]
+    if pad < 1 or pad > 8:
+        raise PaddingError("bad PKCS#7 pad value")
+    if any(b != pad for b in data[-pad:]):
+        raise PaddingError("inconsistent PKCS#7 padding")
+    return bytes(data[:-pad])
+
+
+def _stream(source, sink, ts: TripleSchedule, cfg: DispatchConfig | None, pad: PaddingMode, direction: int):
+    """Run t3des_cu_stream_fd.  `source`/`sink` are int file descriptors or
+    file-like objects (bridged through OS pipes by two helper threads)."""
+    import os
+    import threading
+
+    cfg = cfg or DispatchConfig()
+    if cfg.backend is not Backend.CUDA:
+        raise NotImplementedError("streams run on Backend.CUDA")
+    if cfg.chunk_blocks <= 0:
+        raise ValueError("chunk_blocks must be positive")
+    e = engine(cfg.device)
+    e.set_schedule(ts)
+    e.set_variant(cfg.variant)
+    e.set_launch(0, 0)
+    threads, close_fds, errors = [], [], []
+    if isinstance(source, int):
+        in_fd = source
+    else:
+        r, w = os.pipe()
+        in_fd = r
+        close_fds.append(r)
+
+        def feed():
+            try:
+                while True:
+                    b = source.read(1 << 20)
+                    if not b:
+                        break
+                    _write_all(w, b)
+            except BrokenPipeError:
+                pass
+            except Exception as ex:  # surfaced after the engine returns
+                errors.append(ex)
+            finally:
+                os.close(w)
+
+        threads.append(threading.Thread(target=feed, daemon=True))
+    if isinstance(sink, int):
+        out_fd = sink
+    else:
+        r2, w2 = os.pipe()
+        out_fd = w2
+
+        def drain():
+            try:
+                while True:
+                    b = os.read(r2, 1 << 20)
+                    if not b:
+                        break
+                    sink.write(b)
+            except Exception as ex:
+                errors.append(ex)
+            finally:
+                os.close(r2)
+
+        threads.append(threading.Thread(target=drain, daemon=True))
+    for t in threads:
+        t.start()
+    rep = N.StreamReportC()
+    try:
+        rc = N.lib().t3des_cu_stream_fd(e._h, direction, in_fd, out_fd, cfg.chunk_blocks,
+                                        1 if pad is PaddingMode.PKCS7 else 0, ctypes.byref(rep))
+    finally:
+        if not isinstance(sink, int):
+            os.close(out_fd)
+        for fd in close_fds:
+            os.close(fd)
+        for t in threads:
+            t.join()
+    if errors:
+        raise IoError(str(errors[0]), rep.error_offset)
+    if rc == N.ERR_IO:
+        raise IoError(N.strerror(rc), rep.error_offset)
+    _raise(rc)
+    return StreamReport(rep.bytes_in, rep.bytes_out, rep.chunks, rep.compute_seconds, rep.io_seconds)
+
+
+def _write_all(fd: int, b: bytes) -> None:
+    import os
+
+    mv = memoryview(b)
+    while mv:
+        n = os.write(fd, mv)
+        mv = mv[n:]
+
+
+def encrypt_stream(source, sink, ts: TripleSchedule, cfg: DispatchConfig | None = None,
+                   pad: PaddingMode = PaddingMode.NONE) -> StreamReport:
+    """Chunked ECB encryption of a stream (reference encrypt_stream)."""
+    return _stream(source, sink, ts, cfg, pad, N.ENCRYPT)
+
+
+def decrypt_stream(source, sink, ts: TripleSchedule, cfg: DispatchConfig | None = None,
+                   pad: PaddingMode = PaddingMode.NONE) -> StreamReport:
+    """Chunked ECB decryption of a stream (reference decrypt_stream)."""
+    return _stream(source, sink, ts, cfg, pad, N.DECRYPT)

@@ -18,28 +18,7 @@
 #include "schedule.hpp"
 #include "t3des_cu.h"
 
-struct t3des_cu_ctx {
-    int device = 0;
-    int sms = 0;
-    int bs_occ = 1;           // resident CTAs per SM (occupancy) of the bitsliced kernel
-    int bs_ctas_per_sm = 64;  // grid size of the bitsliced kernel, in CTAs per SM
-    int sp_occ = 1;
-    bool have_schedule = false;
-    int variant = T3DES_CU_VARIANT_BITSLICE;
-    std::size_t chunk_blocks = 0;
-    int work_group = 0;
-    T3BsTable bs[2];
-    T3SpKeyParam sp[2];
-    std::uint32_t* d_sp = nullptr;  // 8x64 fused S/P table (2 KiB)
-    unsigned long long* d_acc = nullptr;
-    static constexpr int kMaxStreams = 8;
-    cudaStream_t st[kMaxStreams] = {};
-    std::uint8_t* buf[kMaxStreams] = {};
-    std::size_t buf_bytes = 0;
-    std::size_t pipe_chunk = std::size_t(32) << 20;  // bytes per pipeline stage
-    int pipe_streams = 3;
-    std::uint64_t launches = 0;
-};
+#include "ctx.hpp"
 
 namespace {
 
@@ -127,10 +106,21 @@ int launch_sptable(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8_
     return T3DES_CU_OK;
 }
 
-// Transform nblocks device blocks (in may equal out), honouring the
-// context's chunk_blocks (blocks per launch).
-int run_device(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8_t* out,
-               std::uint64_t nblocks, cudaStream_t s) {
+int check_batch(t3des_cu_ctx* c, int dir, const void* in, const void* out, std::size_t len) {
+    if (!c || (dir != T3DES_CU_ENCRYPT && dir != T3DES_CU_DECRYPT)) return T3DES_CU_ERR_ARG;
+    if (len % 8) return T3DES_CU_ERR_LENGTH;
+    if (len && (!in || !out)) return T3DES_CU_ERR_ARG;
+    if (partial_overlap(in, out, len)) return T3DES_CU_ERR_OVERLAP;
+    if (!c->have_schedule) return T3DES_CU_ERR_NO_SCHEDULE;
+    return T3DES_CU_OK;
+}
+
+}  // namespace
+
+namespace t3b {
+
+int run_device(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8_t* out, std::uint64_t nblocks,
+               cudaStream_t s) {
     if (nblocks == 0) return T3DES_CU_OK;
     const std::uint64_t step = c->chunk_blocks ? c->chunk_blocks : nblocks;
     for (std::uint64_t off = 0; off < nblocks; off += step) {
@@ -143,16 +133,23 @@ int run_device(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8_t* o
     return T3DES_CU_OK;
 }
 
-int check_batch(t3des_cu_ctx* c, int dir, const void* in, const void* out, std::size_t len) {
-    if (!c || (dir != T3DES_CU_ENCRYPT && dir != T3DES_CU_DECRYPT)) return T3DES_CU_ERR_ARG;
-    if (len % 8) return T3DES_CU_ERR_LENGTH;
-    if (len && (!in || !out)) return T3DES_CU_ERR_ARG;
-    if (partial_overlap(in, out, len)) return T3DES_CU_ERR_OVERLAP;
-    if (!c->have_schedule) return T3DES_CU_ERR_NO_SCHEDULE;
+int ensure_staging(t3des_cu_ctx* c, std::size_t bytes, int n) {
+    bool ok = c->buf_bytes >= bytes;
+    for (int i = 0; i < n && ok; ++i) ok = c->buf[i] != nullptr;
+    if (ok) return T3DES_CU_OK;
+    for (auto& b : c->buf) {
+        if (b) cudaFree(b);
+        b = nullptr;
+    }
+    c->buf_bytes = 0;
+    for (int i = 0; i < n; ++i) T3_CK(cudaMalloc(&c->buf[i], bytes));
+    c->buf_bytes = bytes;
     return T3DES_CU_OK;
 }
 
-}  // namespace
+}  // namespace t3b
+
+using t3b::run_device;
 
 extern "C" {
 
@@ -168,6 +165,8 @@ const char* t3des_cu_strerror(int code) {
         case T3DES_CU_ERR_NO_DEVICE: return "no usable sm_100 CUDA device";
         case T3DES_CU_ERR_CUDA: return "CUDA runtime error";
         case T3DES_CU_ERR_NO_SCHEDULE: return "no key schedule installed";
+        case T3DES_CU_ERR_PADDING: return "malformed PKCS#7 padding";
+        case T3DES_CU_ERR_IO: return "stream read/write failure";
         default: return "unknown error";
     }
 }
@@ -320,15 +319,8 @@ int t3des_cu_ecb_host(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uin
     DeviceScope scope(c->device);
     const std::size_t chunk = std::min(len, c->pipe_chunk);
     const int ns = c->pipe_streams;
-    if (c->buf_bytes < chunk || !c->buf[ns - 1]) {
-        for (auto& b : c->buf) {
-            if (b) cudaFree(b);
-            b = nullptr;
-        }
-        c->buf_bytes = 0;
-        for (int i = 0; i < ns; ++i) T3_CK(cudaMalloc(&c->buf[i], chunk));
-        c->buf_bytes = chunk;
-    }
+    rc = t3b::ensure_staging(c, chunk, ns);
+    if (rc) return rc;
     // Stage k: H2D, kernel, D2H on stream k % ns (in-order per stream, so a
     // stream's buffer is free again when its next stage starts); stages on
     // different streams overlap copies in both directions with kernels.

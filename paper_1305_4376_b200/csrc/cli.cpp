@@ -1,0 +1,487 @@
+// t3des_b200 — command-line front end of the B200 engine, mirroring the
+// reference CLI (/root/reference/proj/tools/t3des_cli.cpp): subcommands
+// encrypt | decrypt | verify | bench, the same flags and the same exit codes
+// (0 ok, 1 I/O, 2 usage, 3 key format, 4 input length, 5 padding, 6 parity,
+// 7 verification failed).  Differences: the backend is "cuda" (the engine
+// has no CPU cipher), --workers counts GPUs, bench sweeps GPU launch shapes.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <iostream>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "t3des_b200/t3des.hpp"
+#include "t3des_cu.h"
+
+namespace {
+
+constexpr int kExitIo = 1, kExitUsage = 2, kExitKeyFormat = 3, kExitInputLength = 4, kExitPadding = 5,
+              kExitParity = 6, kExitVerifyFailed = 7;
+
+struct ParityError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct UsageError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+// ---- key hygiene (reference des.cpp:159-207, CLI-only) -------------------
+bool odd_parity(std::uint64_t k) {
+    for (int i = 0; i < 8; ++i)
+        if (__builtin_popcount(static_cast<unsigned>((k >> (8 * i)) & 0xFF)) % 2 == 0) return false;
+    return true;
+}
+
+bool weak_or_semiweak(std::uint64_t k) {
+    static const std::uint64_t kList[] = {
+        0x0101010101010101ull, 0xFEFEFEFEFEFEFEFEull, 0xE0E0E0E0F1F1F1F1ull, 0x1F1F1F1F0E0E0E0Eull,
+        0x01FE01FE01FE01FEull, 0xFE01FE01FE01FE01ull, 0x1FE01FE00EF10EF1ull, 0xE01FE01FF10EF10Eull,
+        0x01E001E001F101F1ull, 0xE001E001F101F101ull, 0x1FFE1FFE0EFE0EFEull, 0xFE1FFE1FFE0EFE0Eull,
+        0x011F011F010E010Eull, 0x1F011F010E010E01ull, 0xE0FEE0FEF1FEF1FEull, 0xFEE0FEE0FEF1FEF1ull};
+    const std::uint64_t m = 0xFEFEFEFEFEFEFEFEull;  // parity bits masked
+    for (std::uint64_t w : kList)
+        if ((k & m) == (w & m)) return true;
+    return false;
+}
+
+struct Opts {
+    std::string cmd;
+    std::string key_hex, key_file, input = "-", output = "-";
+    bool pkcs7 = false, check_parity = false, strict_keys = false;
+    std::size_t chunk_blocks = 131072, work_group = 256;
+    unsigned workers = 0;
+    std::string backend = "cuda", variant = "bitslice";
+    int device = 0;
+    // bench
+    std::string sweep = "chunk", format = "csv", out, mode = "device";
+    std::vector<std::size_t> values;
+    std::uint64_t payload_mb = 64, seed = 0x3DE5C0DE;
+    unsigned reps = 3;
+};
+
+std::size_t to_size(const std::string& v, const char* flag) {
+    char* end = nullptr;
+    const unsigned long long x = std::strtoull(v.c_str(), &end, 0);
+    if (v.empty() || *end) throw UsageError(std::string("bad value for ") + flag + ": " + v);
+    return static_cast<std::size_t>(x);
+}
+
+Opts parse(int argc, char** argv) {
+    if (argc < 2) throw UsageError("a subcommand is required: encrypt | decrypt | verify | bench");
+    Opts o;
+    o.cmd = argv[1];
+    if (o.cmd == "-h" || o.cmd == "--help") throw UsageError("");
+    if (o.cmd != "encrypt" && o.cmd != "decrypt" && o.cmd != "verify" && o.cmd != "bench")
+        throw UsageError("unknown subcommand: " + o.cmd);
+    const bool crypt = o.cmd == "encrypt" || o.cmd == "decrypt";
+    std::vector<std::string> pos;
+    for (int i = 2; i < argc; ++i) {
+        std::string a = argv[i];
+        auto val = [&](const char* flag) -> std::string {
+            const std::string f(flag);
+            if (a.size() > f.size() && a.compare(0, f.size() + 1, f + "=") == 0) return a.substr(f.size() + 1);
+            if (i + 1 >= argc) throw UsageError(std::string(flag) + " needs a value");
+            return argv[++i];
+        };
+        auto is = [&](const char* flag) { return a == flag || a.rfind(std::string(flag) + "=", 0) == 0; };
+        if (crypt && is("--key")) o.key_hex = val("--key");
+        else if (crypt && is("--key-file")) o.key_file = val("--key-file");
+        else if (crypt && a == "--pkcs7") o.pkcs7 = true;
+        else if (crypt && a == "--check-parity") o.check_parity = true;
+        else if (crypt && a == "--strict-keys") o.strict_keys = true;
+        else if (is("--chunk-blocks")) o.chunk_blocks = to_size(val("--chunk-blocks"), "--chunk-blocks");
+        else if (is("--work-group")) o.work_group = to_size(val("--work-group"), "--work-group");
+        else if (is("--workers")) o.workers = static_cast<unsigned>(to_size(val("--workers"), "--workers"));
+        else if (is("--backend")) o.backend = val("--backend");
+        else if (is("--variant")) o.variant = val("--variant");
+        else if (is("--device")) o.device = static_cast<int>(to_size(val("--device"), "--device"));
+        else if (o.cmd == "bench" && is("--sweep")) o.sweep = val("--sweep");
+        else if (o.cmd == "bench" && is("--values")) {
+            std::string v = val("--values");
+            std::size_t p = 0;
+            while (p <= v.size()) {
+                const std::size_t q = std::min(v.find(',', p), v.size());
+                o.values.push_back(to_size(v.substr(p, q - p), "--values"));
+                p = q + 1;
+            }
+        } else if (o.cmd == "bench" && is("--payload-mb")) o.payload_mb = to_size(val("--payload-mb"), "--payload-mb");
+        else if (o.cmd == "bench" && is("--seed")) o.seed = to_size(val("--seed"), "--seed");
+        else if (o.cmd == "bench" && is("--reps")) o.reps = static_cast<unsigned>(to_size(val("--reps"), "--reps"));
+        else if (o.cmd == "bench" && is("--format")) o.format = val("--format");
+        else if (o.cmd == "bench" && is("--out")) o.out = val("--out");
+        else if (o.cmd == "bench" && is("--mode")) o.mode = val("--mode");
+        else if (!a.empty() && a[0] == '-' && a != "-") throw UsageError("unknown option: " + a);
+        else pos.push_back(a);
+    }
+    if (crypt) {
+        if (pos.size() > 2) throw UsageError("too many positional arguments");
+        if (!pos.empty()) o.input = pos[0];
+        if (pos.size() > 1) o.output = pos[1];
+    } else if (!pos.empty()) {
+        throw UsageError("unexpected argument: " + pos[0]);
+    }
+    if (o.backend != "cuda") throw UsageError("--backend must be cuda (the reference's CPU backends are not in this engine)");
+    if (o.variant != "bitslice" && o.variant != "sptable") throw UsageError("--variant must be bitslice|sptable");
+    if (o.cmd == "bench") {
+        if (o.sweep != "workers" && o.sweep != "chunk" && o.sweep != "workgroup")
+            throw UsageError("--sweep must be workers|chunk|workgroup");
+        if (o.format != "csv" && o.format != "markdown") throw UsageError("--format must be csv|markdown");
+        if (o.mode != "device" && o.mode != "host") throw UsageError("--mode must be device|host");
+        if (o.reps < 1) throw UsageError("--reps must be >= 1");
+    }
+    if (o.chunk_blocks == 0) throw UsageError("--chunk-blocks must be positive");
+    return o;
+}
+
+t3des::TripleKey load_key(const Opts& o) {
+    std::string hex = o.key_hex;
+    if (hex.empty() && !o.key_file.empty()) {
+        std::ifstream in(o.key_file);
+        if (!in) throw t3des::IoError("cannot open key file: " + o.key_file, 0);
+        std::getline(in, hex);
+        while (!hex.empty() && (hex.back() == '\r' || hex.back() == ' ')) hex.pop_back();
+    }
+    if (hex.empty()) throw t3des::KeyFormatError("a key is required (--key or --key-file)");
+    t3des::TripleKey key = t3des::parse_hex_key(hex);
+    for (const t3des::DesKey& k : {key.k1, key.k2, key.k3}) {
+        if (o.check_parity && !odd_parity(k.raw))
+            throw ParityError("key byte fails odd-parity check (--check-parity)");
+        if (weak_or_semiweak(k.raw)) {
+            if (o.strict_keys) throw t3des::KeyFormatError("weak or semi-weak DES key rejected (--strict-keys)");
+            std::cerr << "warning: key component is a weak or semi-weak DES key\n";
+        }
+    }
+    return key;
+}
+
+t3des::DispatchConfig make_config(const Opts& o) {
+    t3des::DispatchConfig cfg;
+    cfg.chunk_blocks = o.chunk_blocks;
+    cfg.work_group = o.work_group;
+    cfg.workers = o.workers;
+    if (cfg.workers == 0)
+        if (const char* env = std::getenv("T3DES_WORKERS")) cfg.workers = static_cast<unsigned>(std::strtoul(env, nullptr, 10));
+    cfg.backend = t3des::Backend::Cuda;
+    cfg.device = o.device;
+    cfg.variant = o.variant == "sptable" ? T3DES_CU_VARIANT_SPTABLE : T3DES_CU_VARIANT_BITSLICE;
+    return cfg;
+}
+
+int run_crypt(const Opts& o, bool encrypt) {
+    const t3des::TripleSchedule ts = t3des::triple_schedule(load_key(o));
+    const t3des::DispatchConfig cfg = make_config(o);
+    const t3des::PaddingMode pad = o.pkcs7 ? t3des::PaddingMode::Pkcs7 : t3des::PaddingMode::None;
+    std::ifstream fin;
+    std::ofstream fout;
+    std::istream* in = &std::cin;
+    std::ostream* out = &std::cout;
+    if (o.input != "-") {
+        fin.open(o.input, std::ios::binary);
+        if (!fin) {
+            std::cerr << "error: cannot open input file: " << o.input << '\n';
+            return kExitIo;
+        }
+        in = &fin;
+    }
+    if (o.output != "-") {
+        fout.open(o.output, std::ios::binary);
+        if (!fout) {
+            std::cerr << "error: cannot open output file: " << o.output << '\n';
+            return kExitIo;
+        }
+        out = &fout;
+    }
+    const t3des::StreamReport r = encrypt ? t3des::encrypt_stream(*in, *out, ts, cfg, pad)
+                                          : t3des::decrypt_stream(*in, *out, ts, cfg, pad);
+    std::cerr << (encrypt ? "encrypted " : "decrypted ") << r.bytes_in << " -> " << r.bytes_out << " bytes, "
+              << r.chunks << " chunks, compute " << r.compute_seconds << " s, io " << r.io_seconds << " s\n";
+    return 0;
+}
+
+// ---- verify: known answers and structural properties, on the GPU --------
+std::vector<std::uint8_t> be(std::uint64_t v) {
+    std::vector<std::uint8_t> b(8);
+    for (int i = 0; i < 8; ++i) b[i] = static_cast<std::uint8_t>(v >> (56 - 8 * i));
+    return b;
+}
+
+int run_verify(const Opts& o) {
+    const t3des::DispatchConfig cfg = make_config(o);
+    bool all = true;
+    auto check = [&](const char* name, bool pass) {
+        std::cout << (pass ? "ok   " : "FAIL ") << name << '\n';
+        all &= pass;
+    };
+    // the classic walkthrough schedule (reference verify.cpp:35-40)
+    const std::uint64_t walk[16] = {0x1B02EFFC7072, 0x79AED9DBC9E5, 0x55FC8A42CF99, 0x72ADD6DB351D,
+                                    0x7CEC07EB53A8, 0x63A53E507B2F, 0xEC84B7F618BC, 0xF78A3AC13BFB,
+                                    0xE0DBEBEDE781, 0xB1F347BA464F, 0x215FD3DED386, 0x7571F59467E9,
+                                    0x97C5D1FABA41, 0x5F43B7F2E73A, 0xBF918D3D3F0A, 0xCB3D8B0E17F5};
+    const auto ks = t3des::key_schedule(t3des::DesKey{0x133457799BBCDFF1ull});
+    check("walkthrough subkeys", std::equal(ks.begin(), ks.end(), walk));
+    struct Kat {
+        const char* key;
+        const char* pt;
+        const char* ct;
+    };
+    // DES vectors as option-3 keys (EDE collapses to DES), TDES vectors for
+    // all keying options and the 3-block NIST SP 800-67 example.
+    const Kat kats[] = {
+        {"133457799BBCDFF1", "0123456789ABCDEF", "85E813540F0AB405"},
+        {"0E329232EA6D0D73", "8787878787878787", "0000000000000000"},
+        {"0101010101010101", "0000000000000000", "8CA64DE9C1B123A7"},
+        {"8001010101010101", "0000000000000000", "95A8D72813DAA94D"},
+        {"7CA110454A1A6E57", "01A1D6D039776742", "690F5B0D9A26939B"},
+        {"0131D9619DC1376E", "5CD54CA83DEF57DA", "7A389D10354BD271"},
+        {"0123456789ABCDEF23456789ABCDEF01456789ABCDEF0123", "5468652071756663", "A826FD8CE53B855F"},
+        {"133457799BBCDFF10E329232EA6D0D737CA110454A1A6E57", "0123456789ABCDEF", "1A493D768C1B9432"},
+        {"0123456789ABCDEF23456789ABCDEF01", "4E6F772069732074", "B7835779EE26ACB7"},
+        {"0123456789ABCDEF", "4E6F772069732074", "3FA40E8A984D4815"},
+        {"0123456789ABCDEF23456789ABCDEF01456789ABCDEF0123",
+         "54686520717566636B2062726F776E20666F78206A756D70",
+         "A826FD8CE53B855FCCE21C8112256FE668D5C05DD9B6B900"},
+    };
+    auto unhex = [](const std::string& h) {
+        std::vector<std::uint8_t> b(h.size() / 2);
+        for (std::size_t i = 0; i < b.size(); ++i) b[i] = static_cast<std::uint8_t>(std::stoul(h.substr(2 * i, 2), nullptr, 16));
+        return b;
+    };
+    bool kat_ok = true;
+    for (const Kat& k : kats) {
+        const auto ts = t3des::triple_schedule(t3des::parse_hex_key(k.key));
+        auto pt = unhex(k.pt), want = unhex(k.ct);
+        std::vector<std::uint8_t> ct(pt.size()), back(pt.size());
+        t3des::encrypt_batch(pt, ct, ts, cfg);
+        t3des::decrypt_batch(ct, back, ts, cfg);
+        kat_ok &= ct == want && back == pt;
+    }
+    check("known-answer vectors (DES via option 3, TDES options 1/2/3, SP 800-67)", kat_ok);
+    // round trips and the complementation property E_{~k}(~x) = ~E_k(x),
+    // 256 random 3-key cases in one batch each
+    std::mt19937_64 rng(0x5EED);
+    bool rt = true, comp = true;
+    for (int i = 0; i < 256; ++i) {
+        t3des::TripleKey key;
+        key.k1.raw = rng();
+        key.k2.raw = rng();
+        key.k3.raw = rng();
+        t3des::TripleKey nkey = key;
+        nkey.k1.raw = ~key.k1.raw;
+        nkey.k2.raw = ~key.k2.raw;
+        nkey.k3.raw = ~key.k3.raw;
+        std::vector<std::uint8_t> x(8 * 33), y(x.size()), z(x.size()), nx(x.size()), ny(x.size());
+        for (auto& b : x) b = static_cast<std::uint8_t>(rng());
+        for (std::size_t j = 0; j < x.size(); ++j) nx[j] = static_cast<std::uint8_t>(~x[j]);
+        const auto ts = t3des::triple_schedule(key);
+        t3des::encrypt_batch(x, y, ts, cfg);
+        t3des::decrypt_batch(y, z, ts, cfg);
+        rt &= z == x;
+        t3des::encrypt_batch(nx, ny, t3des::triple_schedule(nkey), cfg);
+        for (std::size_t j = 0; j < x.size(); ++j) comp &= ny[j] == static_cast<std::uint8_t>(~y[j]);
+    }
+    check("256 random 3-key round trips", rt);
+    check("complementation property", comp);
+    return all ? 0 : kExitVerifyFailed;
+}
+
+// ---- bench: GPU sweeps shaped like the reference's Tables I/II/IV ---------
+struct Rec {
+    unsigned workers;
+    std::size_t chunk, wg;
+    std::uint64_t bytes;
+    double secs = 0, mbs = 0, speedup = 0;
+    bool ok = true;
+};
+
+std::string fmt_double(double v) {
+    char b[32];
+    std::snprintf(b, sizeof b, "%.17g", v);
+    return b;
+}
+
+int run_bench(const Opts& o) {
+    std::vector<std::size_t> values = o.values;
+    if (values.empty()) {
+        if (o.sweep == "workers") values = {1};
+        else if (o.sweep == "chunk") values = {128, 1024, 16384, 131072, 1048576};
+        else values = {32, 64, 128};
+    }
+    for (std::size_t i = 1; i < values.size(); ++i)
+        if (values[i] <= values[i - 1]) throw UsageError("--values must be strictly increasing");
+    const std::uint64_t bytes = o.payload_mb << 20;
+    std::vector<std::uint8_t> payload(bytes);
+    {
+        std::mt19937_64 rng(o.seed);  // reference make_payload layout (bench.cpp:41-51)
+        std::uint64_t w = 0;
+        for (std::uint64_t i = 0; i < bytes; ++i) {
+            if (i % 8 == 0) w = rng();
+            payload[i] = static_cast<std::uint8_t>(w >> (8 * (i % 8)));
+        }
+    }
+    const auto ts = t3des::triple_schedule(t3des::parse_hex_key("133457799BBCDFF10E329232EA6D0D737CA110454A1A6E57"));
+    std::uint64_t sub48[48];
+    std::memcpy(sub48, ts.pass1.data(), 128);
+    std::memcpy(sub48 + 16, ts.pass2.data(), 128);
+    std::memcpy(sub48 + 32, ts.pass3.data(), 128);
+    std::vector<std::uint8_t> first_ct, out(bytes), back(bytes);
+    std::vector<Rec> recs;
+    for (std::size_t v : values) {
+        Rec r{o.workers ? o.workers : 1, o.chunk_blocks, o.work_group, bytes};
+        if (o.sweep == "workers") r.workers = static_cast<unsigned>(v);
+        if (o.sweep == "chunk") r.chunk = v;
+        if (o.sweep == "workgroup") r.wg = v;
+        try {
+            double best = 0;
+            if (o.mode == "device" && r.workers == 1) {
+                t3des_cu_ctx* c = nullptr;
+                int rc = t3des_cu_create(o.device, &c);
+                if (rc) throw std::runtime_error(t3des_cu_strerror(rc));
+                void *din = nullptr, *dout = nullptr;
+                cudaMalloc(&din, bytes);
+                cudaMalloc(&dout, bytes);
+                cudaMemcpy(din, payload.data(), bytes, cudaMemcpyHostToDevice);
+                rc = t3des_cu_set_schedule(c, sub48);
+                if (!rc) rc = t3des_cu_set_variant(c, o.variant == "sptable" ? T3DES_CU_VARIANT_SPTABLE
+                                                                           : T3DES_CU_VARIANT_BITSLICE);
+                if (!rc) rc = t3des_cu_set_launch(c, r.chunk, static_cast<int>(r.wg));
+                cudaEvent_t e0, e1;
+                cudaEventCreate(&e0);
+                cudaEventCreate(&e1);
+                for (unsigned rep = 0; rep <= o.reps && !rc; ++rep) {  // rep 0 = warm-up
+                    cudaEventRecord(e0, nullptr);
+                    rc = t3des_cu_ecb_device(c, T3DES_CU_ENCRYPT, din, dout, bytes, nullptr);
+                    cudaEventRecord(e1, nullptr);
+                    cudaEventSynchronize(e1);
+                    float ms = 0;
+                    cudaEventElapsedTime(&ms, e0, e1);
+                    if (rep > 0 && (rep == 1 || ms * 1e-3 < best)) best = ms * 1e-3;
+                }
+                if (!rc) rc = cudaMemcpy(out.data(), dout, bytes, cudaMemcpyDeviceToHost) ? T3DES_CU_ERR_CUDA : 0;
+                cudaEventDestroy(e0);
+                cudaEventDestroy(e1);
+                cudaFree(din);
+                cudaFree(dout);
+                t3des_cu_destroy(c);
+                if (rc) throw std::runtime_error(t3des_cu_strerror(rc));
+            } else {
+                t3des::DispatchConfig cfg = make_config(o);
+                cfg.workers = r.workers;
+                cfg.chunk_blocks = r.chunk;
+                cfg.work_group = r.wg;
+                cfg.gpu_chunked = true;
+                for (unsigned rep = 0; rep <= o.reps; ++rep) {
+                    const auto t0 = std::chrono::steady_clock::now();
+                    t3des::encrypt_batch(payload, out, ts, cfg);
+                    const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+                    if (rep > 0 && (rep == 1 || s < best)) best = s;
+                }
+            }
+            // every record must decrypt back and agree with the first record
+            t3des::DispatchConfig chk;
+            t3des::decrypt_batch(out, back, ts, chk);
+            if (back != payload) throw std::runtime_error("round trip mismatch");
+            if (first_ct.empty()) first_ct = out;
+            else if (out != first_ct) throw std::runtime_error("launch-shape dependence");
+            r.secs = best;
+            r.mbs = static_cast<double>(bytes) / best / (1 << 20);
+        } catch (const std::exception& e) {
+            std::cerr << "record failed: " << e.what() << '\n';
+            r.ok = false;
+        }
+        recs.push_back(r);
+    }
+    if (!recs.empty() && recs[0].ok)
+        for (Rec& r : recs)
+            if (r.ok) r.speedup = recs[0].secs / r.secs;
+    std::string rep;
+    if (o.format == "csv") {
+        rep = "backend,workers,chunk_blocks,work_group,payload_bytes,compute_seconds,io_seconds,throughput_mb_s,"
+              "speedup_vs_baseline,ok\n";
+        for (const Rec& r : recs)
+            rep += "cuda," + std::to_string(r.workers) + "," + std::to_string(r.chunk) + "," + std::to_string(r.wg) +
+                   "," + std::to_string(r.bytes) + "," + fmt_double(r.secs) + ",0," + fmt_double(r.mbs) + "," +
+                   fmt_double(r.speedup) + "," + (r.ok ? "ok" : "failed") + "\n";
+    } else {
+        rep = "| backend | workers | chunk | work group | payload (B) | compute (s) | io (s) | MB/s | speedup |\n"
+              "|---|---|---|---|---|---|---|---|---|\n";
+        char b[256];
+        for (const Rec& r : recs) {
+            if (r.ok)
+                std::snprintf(b, sizeof b, "| cuda | %u | %zu | %zu | %llu | %.6f | %.4f | %.2f | %.2f |\n", r.workers,
+                              r.chunk, r.wg, (unsigned long long)r.bytes, r.secs, 0.0, r.mbs, r.speedup);
+            else
+                std::snprintf(b, sizeof b, "| cuda | %u | %zu | %zu | failed | - | - | - | - |\n", r.workers, r.chunk,
+                              r.wg);
+            rep += b;
+        }
+    }
+    if (o.out.empty() || o.out == "-") {
+        std::cout << rep;
+    } else {
+        std::ofstream f(o.out);
+        if (!f) {
+            std::cerr << "error: cannot open report file: " << o.out << '\n';
+            return kExitIo;
+        }
+        f << rep;
+    }
+    for (const Rec& r : recs)
+        if (!r.ok) return kExitVerifyFailed;
+    return 0;
+}
+
+const char* kUsage =
+    "usage: t3des_b200 <encrypt|decrypt> [--key HEX | --key-file F] [input|-] [output|-] [--pkcs7]\n"
+    "                  [--check-parity] [--strict-keys] [--chunk-blocks N] [--work-group N]\n"
+    "                  [--workers N] [--backend cuda] [--variant bitslice|sptable] [--device D]\n"
+    "       t3des_b200 verify [--device D]\n"
+    "       t3des_b200 bench [--sweep workers|chunk|workgroup] [--values a,b,...] [--payload-mb M]\n"
+    "                  [--seed S] [--reps R] [--format csv|markdown] [--out F] [--mode device|host]\n";
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    Opts o;
+    try {
+        o = parse(argc, argv);
+    } catch (const UsageError& e) {
+        if (*e.what()) std::cerr << "error: " << e.what() << '\n';
+        std::cerr << kUsage;
+        return (argc >= 2 && (std::strcmp(argv[1], "-h") == 0 || std::strcmp(argv[1], "--help") == 0)) ? 0
+                                                                                                        : kExitUsage;
+    }
+    try {
+        if (o.cmd == "encrypt") return run_crypt(o, true);
+        if (o.cmd == "decrypt") return run_crypt(o, false);
+        if (o.cmd == "verify") return run_verify(o);
+        return run_bench(o);
+    } catch (const t3des::KeyFormatError& e) {
+        std::cerr << "error: " << e.what() << '\n';
+        return kExitKeyFormat;
+    } catch (const t3des::PaddingError& e) {
+        std::cerr << "error: " << e.what() << '\n';
+        return kExitPadding;
+    } catch (const t3des::InputLengthError& e) {
+        std::cerr << "error: " << e.what() << '\n';
+        return kExitInputLength;
+    } catch (const t3des::IoError& e) {
+        std::cerr << "error: " << e.what() << " at byte offset " << e.byte_offset << '\n';
+        return kExitIo;
+    } catch (const ParityError& e) {
+        std::cerr << "error: " << e.what() << '\n';
+        return kExitParity;
+    } catch (const UsageError& e) {
+        std::cerr << "error: " << e.what() << '\n';
+        return kExitUsage;
+    } catch (const std::exception& e) {
+        std::cerr << "error: " << e.what() << '\n';
+        return kExitUsage;
+    }
+}

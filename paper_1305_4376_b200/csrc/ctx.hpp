@@ -1,0 +1,45 @@
+// Private: the engine context behind the C ABI's opaque t3des_cu_ctx and
+// the internal entry points shared by capi.cu and stream.cu.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "t3des_core.cuh"
+#include "t3des_cu.h"
+
+struct t3des_cu_ctx {
+    int device = 0;
+    int sms = 0;
+    int bs_occ = 1;           // resident CTAs per SM (occupancy) of the bitsliced kernel
+    int bs_ctas_per_sm = 64;  // grid size of the bitsliced kernel, in CTAs per SM
+    int sp_occ = 1;
+    bool have_schedule = false;
+    int variant = T3DES_CU_VARIANT_BITSLICE;
+    std::size_t chunk_blocks = 0;
+    int work_group = 0;
+    T3BsTable bs[2];
+    T3SpKeyParam sp[2];
+    std::uint32_t* d_sp = nullptr;  // 8x64 fused S/P table (2 KiB)
+    unsigned long long* d_acc = nullptr;
+    static constexpr int kMaxStreams = 8;
+    cudaStream_t st[kMaxStreams] = {};
+    std::uint8_t* buf[kMaxStreams] = {};
+    std::size_t buf_bytes = 0;
+    std::size_t pipe_chunk = std::size_t(32) << 20;  // bytes per pipeline stage
+    int pipe_streams = 3;
+    std::uint64_t launches = 0;
+};
+
+namespace t3b {
+
+// Transform nblocks device blocks on stream s (in may equal out), honouring
+// the context's variant and launch shaping.  Returns a T3DES_CU_* status.
+int run_device(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8_t* out, std::uint64_t nblocks,
+               cudaStream_t s);
+
+// Make sure the first n staging buffers hold at least `bytes` each.
+int ensure_staging(t3des_cu_ctx* c, std::size_t bytes, int n);
+
+}  // namespace t3b

@@ -28,9 +28,6 @@
 #define T3_OPT_DEFAULT T3_OPT_DFMA  // measured best (profiles/r1/bench_r1c.json variants)
 #endif
 
-struct T3SpKeyParam {
-    uint32_t k[48][8];
-};
 
 // ---- bitsliced kernel --------------------------------------------------
 // VEC = 4: lane t of the warp loads blocks (64j + 2t, 64j + 2t + 1), j < 16,

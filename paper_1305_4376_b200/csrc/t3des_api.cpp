@@ -2,10 +2,13 @@
 #include "t3des_b200/t3des.hpp"
 
 #include <cstring>
+#include <istream>
 #include <map>
 #include <memory>
+#include <ostream>
 
 #include "schedule.hpp"
+#include "stream.hpp"
 #include "t3des_cu.h"
 
 namespace t3des {
@@ -15,6 +18,7 @@ namespace {
     if (rc == T3DES_CU_ERR_LENGTH || rc == T3DES_CU_ERR_OVERLAP)
         throw InputLengthError(t3des_cu_strerror(rc));
     if (rc == T3DES_CU_ERR_KEY) throw KeyFormatError(t3des_cu_strerror(rc));
+    if (rc == T3DES_CU_ERR_PADDING) throw PaddingError(t3des_cu_strerror(rc));
     throw CudaError(std::string("t3des_cu: ") + t3des_cu_strerror(rc), rc);
 }
 
@@ -83,7 +87,79 @@ void run_batch(std::span<const std::uint8_t> in, std::span<std::uint8_t> out, co
     if (rc) raise(rc);
 }
 
+struct IstreamSource : t3b::ByteSource {
+    std::istream& in;
+    explicit IstreamSource(std::istream& s) : in(s) {}
+    std::size_t read(std::uint8_t* dst, std::size_t n) override {
+        in.read(reinterpret_cast<char*>(dst), static_cast<std::streamsize>(n));
+        if (in.bad()) throw std::runtime_error("read failure");
+        return static_cast<std::size_t>(in.gcount());
+    }
+};
+
+struct OstreamSink : t3b::ByteSink {
+    std::ostream& out;
+    explicit OstreamSink(std::ostream& s) : out(s) {}
+    void write(const std::uint8_t* src, std::size_t n) override {
+        out.write(reinterpret_cast<const char*>(src), static_cast<std::streamsize>(n));
+        if (!out) throw std::runtime_error("write failure");
+    }
+    void flush() override { out.flush(); }
+};
+
+StreamReport run_stream(std::istream& source, std::ostream& sink, const TripleSchedule& ts,
+                        const DispatchConfig& cfg, PaddingMode pad, int dir) {
+    if (cfg.backend != Backend::Cuda)
+        throw std::invalid_argument("t3des B200 engine: streams run on Backend::Cuda only");
+    if (cfg.chunk_blocks == 0) throw std::invalid_argument("chunk_blocks must be positive");
+    std::uint64_t sub48[48];
+    flatten(ts, sub48);
+    t3des_cu_ctx* c = context_for(cfg.device);
+    int rc = t3des_cu_set_schedule(c, sub48);
+    if (!rc) rc = t3des_cu_set_variant(c, cfg.variant);
+    if (!rc) rc = t3des_cu_set_launch(c, 0, 0);
+    if (rc) raise(rc);
+    IstreamSource src(source);
+    OstreamSink dst(sink);
+    try {
+        const t3b::StreamStats s = t3b::run_stream(c, dir, src, dst, cfg.chunk_blocks, pad == PaddingMode::Pkcs7);
+        return StreamReport{s.bytes_in, s.bytes_out, s.chunks, s.compute_seconds, s.io_seconds};
+    } catch (const t3b::StreamFailure& f) {
+        switch (f.kind) {
+            case t3b::StreamFailure::Length: throw InputLengthError(f.what());
+            case t3b::StreamFailure::Padding: throw PaddingError(f.what());
+            case t3b::StreamFailure::Io: throw IoError(f.what(), f.byte_offset);
+            default: throw CudaError(f.what(), f.status);
+        }
+    }
+}
+
 }  // namespace
+
+StreamReport encrypt_stream(std::istream& source, std::ostream& sink, const TripleSchedule& ts,
+                            const DispatchConfig& cfg, PaddingMode pad) {
+    return run_stream(source, sink, ts, cfg, pad, T3DES_CU_ENCRYPT);
+}
+
+StreamReport decrypt_stream(std::istream& source, std::ostream& sink, const TripleSchedule& ts,
+                            const DispatchConfig& cfg, PaddingMode pad) {
+    return run_stream(source, sink, ts, cfg, pad, T3DES_CU_DECRYPT);
+}
+
+void pkcs7_pad(std::vector<std::uint8_t>& data) {
+    const std::size_t len = data.size();
+    data.resize(len + 8 - len % 8);
+    std::size_t n = 0;
+    t3b::pkcs7_pad_bytes(data.data(), len, &n);
+}
+
+void pkcs7_unpad(std::vector<std::uint8_t>& data) {
+    try {
+        data.resize(t3b::pkcs7_unpad_len(data.data(), data.size()));
+    } catch (const t3b::StreamFailure& f) {
+        throw PaddingError(f.what());
+    }
+}
 
 TripleKey parse_hex_key(std::string_view hex) {
     std::uint64_t k[3];

@@ -101,6 +101,12 @@ struct T3BsTable {
     uint32_t w[T3_TAB_WORDS];
 };
 
+// Per-round 6-bit key chunks of the SP-table kernel (pre-shifted, see
+// t3b::build_sp_keys).
+struct T3SpKeyParam {
+    uint32_t k[48][8];
+};
+
 // In-register transpose of a 32x32 bit matrix: afterwards x[k] bit m is the
 // old x[m] bit k.  Stages 16 and 8 are byte moves (PRMT); stages 4, 2, 1
 // are mask-select swaps (two shifts + two lop3 per pair).
