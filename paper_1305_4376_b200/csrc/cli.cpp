@@ -55,7 +55,7 @@ struct Opts {
     std::string cmd;
     std::string key_hex, key_file, input = "-", output = "-";
     bool pkcs7 = false, check_parity = false, strict_keys = false;
-    std::size_t chunk_blocks = 131072, work_group = 256;
+    std::size_t chunk_blocks = 131072, work_group = 0;  // work_group: CTA threads, 0 = kernel default
     unsigned workers = 0;
     std::string backend = "cuda", variant = "bitslice";
     int device = 0;
@@ -337,6 +337,7 @@ int run_bench(const Opts& o) {
         if (o.sweep == "workers") r.workers = static_cast<unsigned>(v);
         if (o.sweep == "chunk") r.chunk = v;
         if (o.sweep == "workgroup") r.wg = v;
+        if (r.wg == 0) r.wg = o.variant == "sptable" ? 256 : 128;  // the kernels' own CTA sizes
         try {
             double best = 0;
             if (o.mode == "device" && r.workers == 1) {
