@@ -20,8 +20,9 @@
  * built so far; many randomised restarts keep the smallest circuit.
  * Output: one line per gate, consumed by tools/sboxgen/emit.py.
  *
- * Usage: sboxgen <sbox 0..7> <iterations> <seed> [max_gates [out_file]]
- * (out_file is rewritten each time a smaller circuit is found)
+ * Usage: sboxgen <sbox 0..7> <iterations> <seed> [max_gates [out_file [init_file]]]
+ * (out_file is rewritten each time a smaller circuit is found; with
+ * init_file, run a rip-up-and-rebuild local search from that circuit)
  */
 #include <stdint.h>
 #include <stdio.h>
@@ -376,6 +377,83 @@ static void dump(const char* path, int box, const circ_t* c, const int* outs, co
     if (path) fclose(f);
 }
 
+/* ---- local search: rip up outputs and rebuild them -------------------- */
+static int load_circuit(const char* path, circ_t* c, int* outs) {
+    FILE* f = fopen(path, "r");
+    if (!f) return 0;
+    char line[256];
+    c->n = 6;
+    for (int i = 0; i < 6; i++) {
+        tt_t v = 0;
+        for (int p = 0; p < 64; p++)
+            if ((p >> i) & 1) v |= 1ull << p;
+        c->tt[i] = v;
+    }
+    while (fgets(line, sizeof line, f)) {
+        int g, a, b, cc, o, inv;
+        unsigned lut;
+        if (sscanf(line, "g %d %d %d %d 0x%x", &g, &a, &b, &cc, &lut) == 5) {
+            if (g != c->n) { fclose(f); return 0; }
+            add_gate(c, a, b, cc, (uint8_t)lut);
+        } else if (sscanf(line, "o %d %d %d", &o, &g, &inv) == 3) {
+            outs[o] = g;
+        }
+    }
+    fclose(f);
+    return 1;
+}
+
+static void local_search(int box, long iters, const char* init, const char* out_path, const tt_t* tgt) {
+    circ_t best;
+    int best_out[4];
+    if (!load_circuit(init, &best, best_out)) {
+        fprintf(stderr, "cannot load %s\n", init);
+        exit(2);
+    }
+    fprintf(stderr, "box %d start: %d gates\n", box, best.n - 6);
+    int record = best.n;
+    for (long it = 0; it < iters; it++) {
+        circ_t c = best;
+        int outs[4];
+        memcpy(outs, best_out, sizeof outs);
+        /* rip up 1 or 2 outputs: point them at input 0 so their exclusive
+         * gates become dead, sweep, then rebuild them in random order */
+        int k = (rnd() % 3 == 0) ? 2 : 1;
+        int which[2];
+        which[0] = (int)(rnd() % 4);
+        which[1] = (which[0] + 1 + (int)(rnd() % 3)) % 4;
+        for (int j = 0; j < k; j++) outs[which[j]] = 0;
+        sweep(&c, outs);
+        g_budget = best.n;  /* accept equal cost */
+        g_deep5 = (rnd() & 1);
+        int ok = 1;
+        const int swap = k == 2 && (rnd() & 1);
+        for (int j = 0; j < k && ok; j++) {
+            int o = which[swap ? 1 - j : j];
+            int g = build(&c, tgt[o], ~0ull, 0x3F, 0);
+            if (g < 0) ok = 0;
+            else outs[o] = g;
+        }
+        if (!ok) continue;
+        resub(&c, outs, tgt);
+        int valid = 1;
+        for (int o = 0; o < 4; o++) {
+            tt_t d = c.tt[outs[o]] ^ tgt[o];
+            if (d != 0 && d != ~0ull) valid = 0;
+        }
+        if (!valid) { fprintf(stderr, "internal error: invalid circuit\n"); exit(3); }
+        if (c.n <= best.n) {
+            best = c;
+            memcpy(best_out, outs, sizeof outs);
+            if (c.n < record) {
+                record = c.n;
+                fprintf(stderr, "box %d iter %ld: %d gates\n", box, it, c.n - 6);
+                dump(out_path, box, &best, best_out, tgt);
+            }
+        }
+    }
+}
+
 int main(int argc, char** argv) {
     if (argc < 4) {
         fprintf(stderr, "usage: %s box iterations seed [max_gates]\n", argv[0]);
@@ -389,6 +467,10 @@ int main(int argc, char** argv) {
     const char* out_path = argc > 5 ? argv[5] : NULL;
     tt_t tgt[4];
     for (int o = 0; o < 4; o++) tgt[o] = out_tt(box, o);
+    if (argc > 6) { /* local search from an existing circuit */
+        local_search(box, iters, argv[6], out_path, tgt);
+        return 0;
+    }
     circ_t best;
     int best_out[4] = {0};
     best.n = 1 << 30;
