@@ -69,17 +69,27 @@ int launch_bitslice(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8
                             reinterpret_cast<std::uintptr_t>(out)) & 15u) == 0;
         const bool tma = vec4 && threads == T3_BS_THREADS && c->variant != T3DES_CU_VARIANT_BITSLICE_LDG;
         // tuning variants (A/B measurement of the T3_OPT_* code-generation options)
-        const int opt = c->variant == T3DES_CU_VARIANT_BITSLICE ? T3_OPT_DEFAULT
+        const int opt = c->variant == T3DES_CU_VARIANT_BITSLICE ? c->bs_opt
                         : c->variant == T3DES_CU_VARIANT_BITSLICE_ALU ? 0
                         : c->variant == T3DES_CU_VARIANT_BITSLICE_DFMA ? T3_OPT_DFMA
                                                                        : T3_OPT_SHRFMA;
-        if (tma && opt == 0)
-            t3_bs_tma_kernel<0><<<unsigned(grid), threads, 0, s>>>(in, out, full, c->bs[dir]);
-        else if (tma && (opt & T3_OPT_DFMA))
-            t3_bs_tma_kernel<T3_OPT_DFMA><<<unsigned(grid), threads, 0, s>>>(in, out, full, c->bs[dir]);
-        else if (tma)
-            t3_bs_tma_kernel<T3_OPT_SHRFMA><<<unsigned(grid), threads, 0, s>>>(in, out, full, c->bs[dir]);
-        else if (vec4)
+        if (tma) {
+            switch (opt) {
+#define T3_TMA_CASE(O)                                                                                  \
+    case O:                                                                                             \
+        t3_bs_tma_kernel<O><<<unsigned(grid), threads, 0, s>>>(in, out, full, c->bs[dir]);             \
+        break;
+                T3_TMA_CASE(0)
+                T3_TMA_CASE(1)
+                T3_TMA_CASE(2)
+                T3_TMA_CASE(3)
+                T3_TMA_CASE(5)
+                T3_TMA_CASE(7)
+#undef T3_TMA_CASE
+                default:
+                    return T3DES_CU_ERR_ARG;
+            }
+        } else if (vec4)
             t3_bs_kernel<4, false><<<unsigned(grid), threads, 0, s>>>(in, out, 0, full, nblocks, c->bs[dir]);
         else
             t3_bs_kernel<2, false><<<unsigned(grid), threads, 0, s>>>(in, out, 0, full, nblocks, c->bs[dir]);
@@ -230,6 +240,9 @@ int t3des_cu_create(int device, t3des_cu_ctx** out) {
             break;
         }
         c->bs_occ = std::max(std::min(c->bs_occ, occ_ldg), 1);
+        // Tuning override (experiments only): code-generation options of the
+        // default bitsliced variant (T3_OPT_* mask among the compiled ones).
+        if (const char* e = std::getenv("T3DES_BS_OPT")) c->bs_opt = std::atoi(e);
         // Tuning override (experiments only): grid size in CTAs per SM.
         if (const char* e = std::getenv("T3DES_BS_CTAS_PER_SM")) {
             const int v = std::atoi(e);

@@ -7,6 +7,10 @@
 #include <cstdint>
 
 #include "t3des_core.cuh"
+
+#ifndef T3_OPT_DEFAULT_VALUE
+#define T3_OPT_DEFAULT_VALUE 1  // T3_OPT_DFMA: measured best (profiles/r1)
+#endif
 #include "t3des_cu.h"
 
 struct t3des_cu_ctx {
@@ -14,6 +18,7 @@ struct t3des_cu_ctx {
     int sms = 0;
     int bs_occ = 1;           // resident CTAs per SM (occupancy) of the bitsliced kernel
     int bs_ctas_per_sm = 64;  // grid size of the bitsliced kernel, in CTAs per SM
+    int bs_opt = T3_OPT_DEFAULT_VALUE;  // T3_OPT_* mask of the default bitsliced variant
     int sp_occ = 1;
     bool have_schedule = false;
     int variant = T3DES_CU_VARIANT_BITSLICE;

@@ -25,7 +25,7 @@
 #define T3_SP_THREADS 256
 #define T3_TILE_BLOCKS 1024  // blocks per warp tile (32 lanes x 32 blocks)
 #ifndef T3_OPT_DEFAULT
-#define T3_OPT_DEFAULT T3_OPT_DFMA  // measured best (profiles/r1/bench_r1c.json variants)
+#define T3_OPT_DEFAULT T3_OPT_DFMA  // for the LDG/tail kernels; the TMA kernel's mask is per context
 #endif
 
 

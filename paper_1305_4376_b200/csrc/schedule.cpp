@@ -160,6 +160,11 @@ void build_bitslice_table(const std::uint64_t seq[48], T3BsTable& tab) {
     }
     for (int h = 0; h < 2; ++h)
         for (int q = 0; q < 32; ++q) tab.w[T3_TAB_POST + 32 * h + q] = wh[h][q];
+    // multipliers of the FMA form of the whitening XORs (S = D | 1)
+    for (int i = 0; i < 64; ++i) tab.w[T3_TAB_WS + i] = tab.w[T3_TAB_PRE + i] | 1u;
+    for (int i = 0; i < 32; ++i) tab.w[T3_TAB_WS + 64 + i] = tab.w[T3_TAB_RW1 + i] | 1u;
+    for (int i = 0; i < 32; ++i) tab.w[T3_TAB_WS + 96 + i] = tab.w[T3_TAB_RW2 + i] | 1u;
+    for (int i = 0; i < 64; ++i) tab.w[T3_TAB_WS + 128 + i] = tab.w[T3_TAB_POST + i] | 1u;
 }
 
 void build_sp_keys(const std::uint64_t seq[48], SpKeys& out) {

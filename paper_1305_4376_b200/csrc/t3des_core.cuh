@@ -51,6 +51,7 @@ T3_FI uint32_t prmt(uint32_t a, uint32_t b) {
 enum : int {
     T3_OPT_DFMA = 1,    // E-duplicate key corrections as IMAD (FMA pipe)
     T3_OPT_SHRFMA = 2,  // transpose right shifts as IMAD.HI (FMA pipe)
+    T3_OPT_WFMA = 4,    // pre/re/post whitening XORs as IMAD (FMA pipe)
 };
 
 // x ^ d for a key-correction word d in {0, ~0}.  OPT & DFMA computes it as
@@ -85,7 +86,7 @@ T3_FI uint32_t t3_shr(uint32_t a) {
 #include "generated/bitslice_rounds.cuh"
 
 // ---- whitening/key table (built on the host, schedule.cpp) --------------
-// Word offsets inside the 3264-word table that travels as the kernel's
+// Word offsets inside the 3456-word table that travels as the kernel's
 // __grid_constant__ parameter (constant bank 0, read through LDCU).
 enum : int {
     T3_TAB_PRE = 0,            // 64: initial whitening, half A then half B
@@ -94,7 +95,8 @@ enum : int {
     T3_TAB_RW1 = 64 + 48 * T3_ROUND_WORDS, // 32: re-whitening of A between pass 1 and 2
     T3_TAB_RW2 = T3_TAB_RW1 + 32,  // 32: re-whitening of B between pass 2 and 3
     T3_TAB_POST = T3_TAB_RW2 + 32, // 64: final un-whitening, A then B
-    T3_TAB_WORDS = T3_TAB_POST + 64,
+    T3_TAB_WS = T3_TAB_POST + 64,  // 192: S = D | 1 for PRE(64), RW1(32), RW2(32), POST(64)
+    T3_TAB_WORDS = T3_TAB_WS + 192,
 };
 
 struct T3BsTable {
@@ -147,10 +149,11 @@ T3_FI void t3_transpose32(uint32_t (&x)[32]) {
     }
 }
 
-template <class KP>
-T3_FI void t3_xor_table(uint32_t (&h)[32], const KP k) {
+// h ^= table words k (0/~0); with WFMA as IMAD h*s+k, s = the matching S words.
+template <int OPT, class KP>
+T3_FI void t3_xor_table(uint32_t (&h)[32], const KP k, const KP s) {
 #pragma unroll
-    for (int q = 0; q < 32; ++q) h[q] ^= k[q];
+    for (int q = 0; q < 32; ++q) h[q] = (OPT & T3_OPT_WFMA) ? t3_dfix<T3_OPT_DFMA>(h[q], k[q], s[q]) : (h[q] ^ k[q]);
 }
 
 // All 48 rounds (3 passes of 16) on halves A (initial L) and B (initial R).
@@ -158,27 +161,27 @@ T3_FI void t3_xor_table(uint32_t (&h)[32], const KP k) {
 // renamings: pass 2 runs with the roles of A and B exchanged.
 template <int OPT, class KP>
 T3_FI void t3_cipher(uint32_t (&A)[32], uint32_t (&B)[32], const KP w) {
-    t3_xor_table(A, w + T3_TAB_PRE);
-    t3_xor_table(B, w + T3_TAB_PRE + 32);
+    t3_xor_table<OPT>(A, w + T3_TAB_PRE, w + T3_TAB_WS);
+    t3_xor_table<OPT>(B, w + T3_TAB_PRE + 32, w + T3_TAB_WS + 32);
 #pragma unroll 1
     for (int it = 0; it < 8; ++it) {
         t3_round<OPT>(A, B, w + T3_TAB_ROUND + (2 * it) * T3_ROUND_WORDS);
         t3_round<OPT>(B, A, w + T3_TAB_ROUND + (2 * it + 1) * T3_ROUND_WORDS);
     }
-    t3_xor_table(A, w + T3_TAB_RW1);
+    t3_xor_table<OPT>(A, w + T3_TAB_RW1, w + T3_TAB_WS + 64);
 #pragma unroll 1
     for (int it = 0; it < 8; ++it) {
         t3_round<OPT>(B, A, w + T3_TAB_ROUND + (16 + 2 * it) * T3_ROUND_WORDS);
         t3_round<OPT>(A, B, w + T3_TAB_ROUND + (17 + 2 * it) * T3_ROUND_WORDS);
     }
-    t3_xor_table(B, w + T3_TAB_RW2);
+    t3_xor_table<OPT>(B, w + T3_TAB_RW2, w + T3_TAB_WS + 96);
 #pragma unroll 1
     for (int it = 0; it < 8; ++it) {
         t3_round<OPT>(A, B, w + T3_TAB_ROUND + (32 + 2 * it) * T3_ROUND_WORDS);
         t3_round<OPT>(B, A, w + T3_TAB_ROUND + (33 + 2 * it) * T3_ROUND_WORDS);
     }
-    t3_xor_table(A, w + T3_TAB_POST);
-    t3_xor_table(B, w + T3_TAB_POST + 32);
+    t3_xor_table<OPT>(A, w + T3_TAB_POST, w + T3_TAB_WS + 128);
+    t3_xor_table<OPT>(B, w + T3_TAB_POST + 32, w + T3_TAB_WS + 160);
 }
 
 // One thread's 32 blocks: lo[m]/hi[m] are the little-endian words holding

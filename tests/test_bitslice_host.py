@@ -72,8 +72,18 @@ def test_whitening_table_primary_slots(oracle):
     s = oracle.schedule_hex(KEYS[0])
     w = (ctypes.c_uint32 * 8192)()
     nw = lib.bs_host_table(s, 0, w)
-    stride = (nw - 64 - 128) // 48  # words per round
-    w = np.array(w[:nw], dtype=np.uint64) & 1
+    # layout (t3des_core.cuh T3_TAB_*): PRE 64 | 48 rounds x 64 | RW1 32 | RW2 32 | POST 64 | S words 192
+    stride = 64
+    rw1 = 64 + 48 * stride
+    rw2, post, ws = rw1 + 32, rw1 + 64, rw1 + 128
+    assert nw == ws + 192
+    w = np.array(w[:nw], dtype=np.uint64)
+    for dst, src, n in ((ws, 0, 64), (ws + 64, rw1, 32), (ws + 96, rw2, 32), (ws + 128, post, 64)):
+        assert np.array_equal(w[dst:dst + n], w[src:src + n] | 1)  # FMA multipliers S = D | 1
+    for t in range(48):
+        d = w[64 + stride * t + 32: 64 + stride * t + 48]
+        assert np.array_equal(w[64 + stride * t + 48: 64 + stride * t + 64], d | 1)
+    w = w & 1
     seq = [s[i] for i in range(16)] + [s[31 - i] for i in range(16)] + [s[32 + i] for i in range(16)]
     prim = G.e_slot_maps()[0]
 
@@ -86,13 +96,13 @@ def test_whitening_table_primary_slots(oracle):
         lh = (loc % 2) if p != 1 else 1 - (loc % 2)
         rh = 1 - lh
         if t == 16:
-            wh[0] ^= w[nw - 128: nw - 96]
+            wh[0] ^= w[rw1: rw1 + 32]
         if t == 32:
-            wh[1] ^= w[nw - 96: nw - 64]
+            wh[1] ^= w[rw2: rw2 + 32]
         assert np.array_equal(wh[rh], kp(t)), t
         wh[lh] ^= w[64 + stride * t: 64 + stride * t + 32]
-    wh[0] ^= w[nw - 64: nw - 32]
-    wh[1] ^= w[nw - 32: nw]
+    wh[0] ^= w[post: post + 32]
+    wh[1] ^= w[post + 32: post + 64]
     assert not wh[0].any() and not wh[1].any()
 
 
