@@ -75,6 +75,8 @@ typedef struct {
 
 static int g_budget = 40;  /* max gates (including the 6 inputs) */
 static int g_deep5 = 1;    /* enable the 2-gate search */
+static int g_deep5_depth = 1;  /* ... down to this recursion depth */
+static int g_gate_sel = 0;     /* internal gates tried as mux selectors at depth 0 */
 static uint64_t g_rng = 88172645463325252ull;
 
 static uint64_t rnd(void) {
@@ -216,7 +218,7 @@ static int build(circ_t* st, tt_t T, tt_t M, int avail, int depth) {
         }
     }
     if (st->n + 2 > g_budget) return -1;
-    if (g_deep5 && depth <= 1) {
+    if (g_deep5 && depth <= g_deep5_depth) {
         int g = search5(st, T, M);
         if (g >= 0) return g;
     }
@@ -225,7 +227,7 @@ static int build(circ_t* st, tt_t T, tt_t M, int avail, int depth) {
     circ_t best;
     int best_g = -1;
     best.n = 1 << 30;
-    int order[6], cnt = 0;
+    int order[6 + MAXG], cnt = 0;
     for (int s = 0; s < 6; s++)
         if (avail & (1 << s)) order[cnt++] = s;
     for (int i = cnt - 1; i > 0; i--) {
@@ -233,15 +235,20 @@ static int build(circ_t* st, tt_t T, tt_t M, int avail, int depth) {
         int t = order[i]; order[i] = order[j]; order[j] = t;
     }
     int tries = depth == 0 ? cnt : (depth == 1 ? (cnt < 3 ? cnt : 3) : 1);
+    if (depth == 0 && g_gate_sel > 0 && st->n > 6) {
+        /* also split on existing internal signals (keeps `avail`) */
+        for (int k = 0; k < g_gate_sel; k++) order[tries++] = 6 + (int)(rnd() % (unsigned)(st->n - 6));
+    }
     for (int si = 0; si < tries; si++) {
         int s = order[si];
+        const int drop = s < 6 ? (1 << s) : 0;
         tt_t S = st->tt[s];
         for (int first = 0; first < 2; first++) {
             tt_t M0 = first == 0 ? (M & ~S) : (M & S);
             tt_t M1 = M & ~M0;
             for (int variant = 0; variant < 3; variant++) {
                 circ_t c = *st;
-                int f0 = build(&c, T, M0, avail & ~(1 << s), depth + 1);
+                int f0 = build(&c, T, M0, avail & ~drop, depth + 1);
                 if (f0 < 0) continue;
                 tt_t F0 = c.tt[f0];
                 tt_t T1 = T, MM1 = M1;
@@ -266,7 +273,7 @@ static int build(circ_t* st, tt_t T, tt_t M, int avail, int depth) {
                         continue;
                     }
                 }
-                int f1 = build(&c, T1, MM1, avail & ~(1 << s), depth + 1);
+                int f1 = build(&c, T1, MM1, avail & ~drop, depth + 1);
                 if (f1 < 0) continue;
                 if (c.n >= g_budget) continue;
                 uint8_t l;
@@ -426,6 +433,8 @@ static void local_search(int box, long iters, const char* init, const char* out_
         sweep(&c, outs);
         g_budget = best.n;  /* accept equal cost */
         g_deep5 = (rnd() & 1);
+        g_deep5_depth = 1 + (int)(rnd() % 3);
+        g_gate_sel = (int)(rnd() % 4);
         int ok = 1;
         const int swap = k == 2 && (rnd() & 1);
         for (int j = 0; j < k && ok; j++) {
@@ -488,6 +497,8 @@ int main(int argc, char** argv) {
         g_budget = (best.n < (1 << 30) ? best.n - 1 : cap);
         if (g_budget > cap) g_budget = cap;
         g_deep5 = (rnd() & 3) != 0;
+        g_deep5_depth = 1 + (int)(rnd() % 3);
+        g_gate_sel = (int)(rnd() % 4);
         int ord[4] = {0, 1, 2, 3};
         for (int i = 3; i > 0; i--) {
             int j = (int)(rnd() % (unsigned)(i + 1));
