@@ -252,3 +252,48 @@ int main(int argc, char** argv) {
     subprocess.check_call([str(exe), KEYS[0], str(outp)])
     x = (np.arange(8 * 8195, dtype=np.uint64) * 131 + 7).astype(np.uint8)
     assert outp.read_bytes() == oracle.ecb(x, oracle.schedule_hex(KEYS[0]), 0).tobytes()
+
+
+def test_64gib_sharding_invariance_on_one_device(eng, oracle):
+    """BASELINE configs[3]: 64 GiB encrypted as G = 1, 2, 4, 8 block-range
+    shards (t3des_cu_shard_range — the split ecb_multi and bench.py's ranks
+    use), here run one after another on one B200 in place.  The ciphertext
+    checksum must not depend on G, decrypt must restore the payload, and
+    sampled blocks (incl. every shard edge) must match the oracle."""
+    from paper_1305_4376_b200.sharding import shard_range
+
+    free, _ = torch.cuda.mem_get_info()
+    n = (64 << 30) // 8
+    if free < 8 * n + (4 << 30):
+        pytest.skip("needs ~68 GiB of free device memory")
+    ts = t3.triple_schedule(t3.parse_hex_key(BENCH_KEY))
+    s = oracle.schedule_hex(BENCH_KEY)
+    buf = torch.empty(8 * n, dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    eng.set_schedule(ts)
+    eng.set_variant(N.VARIANT_BITSLICE)
+    eng.set_launch(0, 0)
+    eng.fill_splitmix(buf.data_ptr(), 0, n, 0xC0FFEE, st)
+    cs_plain = eng.checksum(buf.data_ptr(), 0, n, st)
+    sums = {}
+    edges = set()
+    for g in (1, 2, 4, 8):
+        for r in range(g):
+            first, count = shard_range(n, g, r)
+            edges.update((first, max(first + count - 1, 0)))
+            eng.ecb_device(0, buf.data_ptr() + 8 * first, buf.data_ptr() + 8 * first, 8 * count, st)
+        # per-shard checksums add up to the whole
+        tot = 0
+        for r in range(g):
+            first, count = shard_range(n, g, r)
+            tot = (tot + eng.checksum(buf.data_ptr() + 8 * first, first, count, st)) % 2**64
+        sums[g] = tot
+        if g == 1:
+            rng = np.random.default_rng(64)
+            idx = np.unique(np.concatenate([rng.integers(0, n, 1000), sorted(edges)])).astype(np.int64)
+            got = buf.view(torch.int64)[torch.from_numpy(idx).cuda()].cpu().numpy().view(np.uint8)
+            src = np.concatenate([oracle.splitmix(int(i), 1, 0xC0FFEE) for i in idx])
+            assert np.array_equal(got, oracle.ecb(src, s, 0))
+        eng.ecb_device(1, buf.data_ptr(), buf.data_ptr(), 8 * n, st)  # back to plaintext
+        assert eng.checksum(buf.data_ptr(), 0, n, st) == cs_plain
+    assert len(set(sums.values())) == 1, sums
