@@ -268,6 +268,35 @@ def extra_configs(e, orc, t3, N, torch, np) -> dict:
                               "note": "device: 5 decrypts of the 4 GiB ciphertext, CUDA events; "
                                       "e2e: t3des_cu_ecb_host pinned in -> pinned out incl. H2D/D2H"}
     del host
+    # configs[3]: 64 GiB in block-range shards; on one device the G shards
+    # run back to back (the torchrun bench runs them on G GPUs)
+    from paper_1305_4376_b200.sharding import shard_range
+
+    n64 = (64 << 30) // 8
+    free, _ = torch.cuda.mem_get_info()
+    if free >= 8 * n64 + (4 << 30):
+        big = torch.empty(8 * n64, dtype=torch.uint8, device="cuda")
+        e.fill_splitmix(big.data_ptr(), 0, n64, SEED, stream)
+        sums, times = {}, {}
+        for g in (1, 8):
+            e.ecb_device(1, big.data_ptr(), big.data_ptr(), 8 * n64, stream)  # warm / restore alternation
+            e.ecb_device(0, big.data_ptr(), big.data_ptr(), 8 * n64, stream)
+            torch.cuda.synchronize()
+            ev0.record()
+            for r in range(g):
+                first, count = shard_range(n64, g, r)
+                e.ecb_device(1, big.data_ptr() + 8 * first, big.data_ptr() + 8 * first, 8 * count, stream)
+            ev1.record()
+            torch.cuda.synchronize()
+            times[g] = ev0.elapsed_time(ev1)
+            sums[g] = e.checksum(big.data_ptr(), 0, n64, stream)
+        out["c3_64GiB_block_range_shards"] = {
+            "device_GBps_1_shard": round(8 * n64 / times[1] / 1e6, 2),
+            "device_GBps_8_shards_back_to_back": round(8 * n64 / times[8] / 1e6, 2),
+            "checksum_equal_1_vs_8_shards": sums[1] == sums[8],
+            "note": "in-place decrypt of 64 GiB on one B200; the 8 shard ranges are the ones 8 GPUs would own"}
+        del big
+        torch.cuda.empty_cache()
     return out
 
 
