@@ -278,9 +278,9 @@ def extra_configs(e, orc, t3, N, torch, np) -> dict:
         big = torch.empty(8 * n64, dtype=torch.uint8, device="cuda")
         e.fill_splitmix(big.data_ptr(), 0, n64, SEED, stream)
         sums, times = {}, {}
-        for g in (1, 8):
-            e.ecb_device(1, big.data_ptr(), big.data_ptr(), 8 * n64, stream)  # warm / restore alternation
-            e.ecb_device(0, big.data_ptr(), big.data_ptr(), 8 * n64, stream)
+        e.ecb_device(1, big.data_ptr(), big.data_ptr(), 8 * n64, stream)  # warm-up pair
+        e.ecb_device(0, big.data_ptr(), big.data_ptr(), 8 * n64, stream)
+        for g in (1, 8):  # each g: decrypt the payload P in g shard ranges, checksum, restore P
             torch.cuda.synchronize()
             ev0.record()
             for r in range(g):
@@ -290,6 +290,7 @@ def extra_configs(e, orc, t3, N, torch, np) -> dict:
             torch.cuda.synchronize()
             times[g] = ev0.elapsed_time(ev1)
             sums[g] = e.checksum(big.data_ptr(), 0, n64, stream)
+            e.ecb_device(0, big.data_ptr(), big.data_ptr(), 8 * n64, stream)
         out["c3_64GiB_block_range_shards"] = {
             "device_GBps_1_shard": round(8 * n64 / times[1] / 1e6, 2),
             "device_GBps_8_shards_back_to_back": round(8 * n64 / times[8] / 1e6, 2),

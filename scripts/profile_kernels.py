@@ -9,7 +9,7 @@ import torch  # noqa: E402
 
 import paper_1305_4376_b200 as t3  # noqa: E402
 
-n = (1 << 30) // 8
+n = (int(os.environ.get("T3_GIB", "1")) << 30) // 8
 e = t3.Engine(0)
 e.set_schedule(t3.triple_schedule(t3.parse_hex_key("133457799BBCDFF10E329232EA6D0D737CA110454A1A6E57")))
 src = torch.empty(8 * n, dtype=torch.uint8, device="cuda")
