@@ -62,8 +62,13 @@ int launch_bitslice(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8
         // hardware CTA scheduler then balances the SMs and de-phases the
         // warps' load/compute cycles (measured: 2.87 ms vs 3.02 ms for a
         // persistent 4-CTA/SM grid on 1 GiB, scripts/grid_sweep.sh).
-        const std::uint64_t cap = std::uint64_t(c->sms) * std::uint64_t(c->bs_ctas_per_sm) *
-                                  (T3_BS_THREADS / 32) / warps_per_cta;
+        // ... and it scales with the batch (about kTilesPerWarp tiles per warp)
+        // so that warps never live long enough to fall into lockstep.
+        constexpr std::uint64_t kTilesPerWarp = 4;
+        const std::uint64_t cap =
+            std::max<std::uint64_t>(std::uint64_t(c->sms) * std::uint64_t(c->bs_ctas_per_sm) *
+                                        (T3_BS_THREADS / 32) / warps_per_cta,
+                                    full / (warps_per_cta * kTilesPerWarp));
         grid = std::min<std::uint64_t>(grid, std::max<std::uint64_t>(cap, 1));
         const bool vec4 = ((reinterpret_cast<std::uintptr_t>(in) |
                             reinterpret_cast<std::uintptr_t>(out)) & 15u) == 0;
