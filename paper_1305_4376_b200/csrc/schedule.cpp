@@ -1,6 +1,7 @@
 // Host keying for the B200 3DES engine (see schedule.hpp).
 #include "schedule.hpp"
 
+#include <cstdlib>
 #include <cstring>
 
 #include "generated/bitslice_tables.h"
@@ -160,6 +161,11 @@ void build_bitslice_table(const std::uint64_t seq[48], T3BsTable& tab) {
     }
     for (int h = 0; h < 2; ++h)
         for (int q = 0; q < 32; ++q) tab.w[T3_TAB_POST + 32 * h + q] = wh[h][q];
+    // The kernel skips the XORs that are zero by construction: half A's
+    // initial whitening (A is written before it is read) and half B's final
+    // one (B is not read after the last round).
+    for (int q = 0; q < 32; ++q)
+        if (tab.w[T3_TAB_PRE + q] != 0 || tab.w[T3_TAB_POST + 32 + q] != 0) std::abort();
     // multipliers of the FMA form of the whitening XORs (S = D | 1)
     for (int i = 0; i < 64; ++i) tab.w[T3_TAB_WS + i] = tab.w[T3_TAB_PRE + i] | 1u;
     for (int i = 0; i < 32; ++i) tab.w[T3_TAB_WS + 64 + i] = tab.w[T3_TAB_RW1 + i] | 1u;

@@ -161,7 +161,8 @@ T3_FI void t3_xor_table(uint32_t (&h)[32], const KP k, const KP s) {
 // renamings: pass 2 runs with the roles of A and B exchanged.
 template <int OPT, class KP>
 T3_FI void t3_cipher(uint32_t (&A)[32], uint32_t (&B)[32], const KP w) {
-    t3_xor_table<OPT>(A, w + T3_TAB_PRE, w + T3_TAB_WS);
+    // A is written (round 1) before it is ever read, so its initial whitening
+    // is 0 by construction (checked in build_bitslice_table); only B needs it.
     t3_xor_table<OPT>(B, w + T3_TAB_PRE + 32, w + T3_TAB_WS + 32);
 #pragma unroll 1
     for (int it = 0; it < 8; ++it) {
@@ -180,8 +181,9 @@ T3_FI void t3_cipher(uint32_t (&A)[32], uint32_t (&B)[32], const KP w) {
         t3_round<OPT>(A, B, w + T3_TAB_ROUND + (32 + 2 * it) * T3_ROUND_WORDS);
         t3_round<OPT>(B, A, w + T3_TAB_ROUND + (33 + 2 * it) * T3_ROUND_WORDS);
     }
+    // B is never read after round 48, so its final whitening is 0 (checked
+    // on the host); only A is un-whitened.
     t3_xor_table<OPT>(A, w + T3_TAB_POST, w + T3_TAB_WS + 128);
-    t3_xor_table<OPT>(B, w + T3_TAB_POST + 32, w + T3_TAB_WS + 160);
 }
 
 // One thread's 32 blocks: lo[m]/hi[m] are the little-endian words holding
