@@ -230,7 +230,7 @@ int t3des_cu_create(int device, t3des_cu_ctx** out) {
     int rc = T3DES_CU_OK;
     do {
         int occ_ldg = 1;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->bs_occ, t3_bs_tma_kernel<T3_OPT_DEFAULT>, T3_BS_THREADS, 0) !=
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->bs_occ, t3_bs_tma_kernel<T3_OPT_DEFAULT_VALUE>, T3_BS_THREADS, 0) !=
                 cudaSuccess ||
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_ldg, t3_bs_kernel<4, false>, T3_BS_THREADS, 0) !=
                 cudaSuccess) {

@@ -9,7 +9,7 @@
 #include "t3des_core.cuh"
 
 #ifndef T3_OPT_DEFAULT_VALUE
-#define T3_OPT_DEFAULT_VALUE 1  // T3_OPT_DFMA: measured best (profiles/r1)
+#define T3_OPT_DEFAULT_VALUE 5  // T3_OPT_DFMA | T3_OPT_WFMA: measured best (scripts/opt_sweep.sh)
 #endif
 #include "t3des_cu.h"
 
