@@ -75,9 +75,16 @@ class ClockSampler:
             import pynvml
 
             pynvml.nvmlInit()
-            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
-            idx = int(vis.split(",")[self.device]) if vis else self.device
-            h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            h = None
+            try:  # CUDA and NVML orderings can differ: match by UUID
+                import torch
+
+                uuid = str(torch.cuda.get_device_properties(self.device).uuid)
+                h = pynvml.nvmlDeviceGetHandleByUUID(("GPU-" + uuid) if not uuid.startswith("GPU-") else uuid)
+            except Exception:
+                vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+                idx = int(vis.split(",")[self.device]) if vis else self.device
+                h = pynvml.nvmlDeviceGetHandleByIndex(idx)
             self._nvml = (pynvml, h)
             self._t = threading.Thread(target=self._loop, daemon=True)
             self._t.start()
