@@ -99,7 +99,7 @@ struct DispatchConfig {
     unsigned workers = 0;               // CUDA: number of GPUs (0 = 1, device `device`)
     Backend backend = Backend::Cuda;
     int device = 0;                     // first CUDA device
-    int variant = 0;                    // 0 bitsliced (default), 1 SP-table
+    int variant = 6;                    // T3DES_CU_VARIANT_*: 6 auto (default), 0 bitsliced, 1 SP-table
     bool gpu_chunked = false;           // apply chunk_blocks/work_group to launches
 };
 

@@ -48,13 +48,18 @@ extern "C" {
 #define T3DES_CU_ENCRYPT 0
 #define T3DES_CU_DECRYPT 1
 
-#define T3DES_CU_VARIANT_BITSLICE 0     /* bitsliced lop3 kernel, TMA tile prefetch (default) */
+#define T3DES_CU_VARIANT_BITSLICE 0     /* bitsliced lop3 kernel, TMA tile prefetch           */
 #define T3DES_CU_VARIANT_SPTABLE 1      /* shared-memory SP-table kernel                      */
 #define T3DES_CU_VARIANT_BITSLICE_LDG 2 /* bitsliced, direct LDG loads (kept for measurement) */
 /* Tuning variants of the bitsliced + TMA kernel (A/B measurement only):   */
 #define T3DES_CU_VARIANT_BITSLICE_ALU 3    /* all key/shift work on the ALU pipe    */
 #define T3DES_CU_VARIANT_BITSLICE_DFMA 4   /* E-duplicate key XORs as IMAD          */
 #define T3DES_CU_VARIANT_BITSLICE_SHRFMA 5 /* transpose right shifts as IMAD.HI     */
+/* Default: bitsliced, except launches of <= T3DES_CU_AUTO_SMALL_BLOCKS blocks,
+ * which go to the SP-table kernel (lower latency: one thread per block instead
+ * of one warp per 1024 blocks; measured crossover ~1 MiB). */
+#define T3DES_CU_VARIANT_AUTO 6
+#define T3DES_CU_AUTO_SMALL_BLOCKS 131072
 
 typedef struct t3des_cu_ctx t3des_cu_ctx;
 
@@ -87,7 +92,7 @@ int t3des_cu_destroy(t3des_cu_ctx* ctx);
  * (tdes.cpp:177-185) and the kernels' constant tables; no device traffic. */
 int t3des_cu_set_schedule(t3des_cu_ctx* ctx, const uint64_t sub48[48]);
 
-/* T3DES_CU_VARIANT_*; default BITSLICE. */
+/* T3DES_CU_VARIANT_*; default AUTO. */
 int t3des_cu_set_variant(t3des_cu_ctx* ctx, int variant);
 
 /* Launch shaping, the GPU reading of DispatchConfig (dispatch.hpp:25-30):

@@ -4,6 +4,7 @@ Host API mirroring the reference's t3des API; the cipher runs only in the
 CUDA kernels of libt3des_b200.so.
 """
 from ._native import (  # noqa: F401
+    VARIANT_AUTO,
     DECRYPT,
     ENCRYPT,
     VARIANT_BITSLICE,

@@ -33,6 +33,8 @@ VARIANT_BITSLICE_LDG = 2
 VARIANT_BITSLICE_ALU = 3
 VARIANT_BITSLICE_DFMA = 4
 VARIANT_BITSLICE_SHRFMA = 5
+VARIANT_AUTO = 6
+AUTO_SMALL_BLOCKS = 131072
 
 class StreamReportC(ctypes.Structure):
     """t3des_cu_stream_report (include/t3des_cu.h)."""

@@ -162,7 +162,7 @@ class DispatchConfig:
     workers: int = 0            # CUDA: number of GPUs (0 = one, `device`)
     backend: Backend = Backend.CUDA
     device: int = 0
-    variant: int = N.VARIANT_BITSLICE
+    variant: int = N.VARIANT_AUTO
     gpu_chunked: bool = False
 
 

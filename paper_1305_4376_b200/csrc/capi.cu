@@ -74,7 +74,7 @@ int launch_bitslice(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8
                             reinterpret_cast<std::uintptr_t>(out)) & 15u) == 0;
         const bool tma = vec4 && threads == T3_BS_THREADS && c->variant != T3DES_CU_VARIANT_BITSLICE_LDG;
         // tuning variants (A/B measurement of the T3_OPT_* code-generation options)
-        const int opt = c->variant == T3DES_CU_VARIANT_BITSLICE ? c->bs_opt
+        const int opt = (c->variant == T3DES_CU_VARIANT_BITSLICE || c->variant == T3DES_CU_VARIANT_AUTO) ? c->bs_opt
                         : c->variant == T3DES_CU_VARIANT_BITSLICE_ALU ? 0
                         : c->variant == T3DES_CU_VARIANT_BITSLICE_DFMA ? T3_OPT_DFMA
                                                                        : T3_OPT_SHRFMA;
@@ -140,9 +140,10 @@ int run_device(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8_t* o
     const std::uint64_t step = c->chunk_blocks ? c->chunk_blocks : nblocks;
     for (std::uint64_t off = 0; off < nblocks; off += step) {
         const std::uint64_t n = std::min(step, nblocks - off);
-        const int rc = c->variant == T3DES_CU_VARIANT_SPTABLE
-                           ? launch_sptable(c, dir, in + 8 * off, out + 8 * off, n, s)
-                           : launch_bitslice(c, dir, in + 8 * off, out + 8 * off, n, s);
+        const bool sp = c->variant == T3DES_CU_VARIANT_SPTABLE ||
+                        (c->variant == T3DES_CU_VARIANT_AUTO && n <= T3DES_CU_AUTO_SMALL_BLOCKS);
+        const int rc = sp ? launch_sptable(c, dir, in + 8 * off, out + 8 * off, n, s)
+                          : launch_bitslice(c, dir, in + 8 * off, out + 8 * off, n, s);
         if (rc) return rc;
     }
     return T3DES_CU_OK;
@@ -305,7 +306,7 @@ int t3des_cu_set_schedule(t3des_cu_ctx* c, const std::uint64_t sub48[48]) {
 }
 
 int t3des_cu_set_variant(t3des_cu_ctx* c, int variant) {
-    if (!c || variant < T3DES_CU_VARIANT_BITSLICE || variant > T3DES_CU_VARIANT_BITSLICE_SHRFMA)
+    if (!c || variant < T3DES_CU_VARIANT_BITSLICE || variant > T3DES_CU_VARIANT_AUTO)
         return T3DES_CU_ERR_ARG;
     c->variant = variant;
     return T3DES_CU_OK;
@@ -313,7 +314,8 @@ int t3des_cu_set_variant(t3des_cu_ctx* c, int variant) {
 
 int t3des_cu_set_launch(t3des_cu_ctx* c, std::size_t chunk_blocks, int work_group) {
     if (!c || work_group < 0 || work_group > 1024 || (work_group % 32) != 0) return T3DES_CU_ERR_ARG;
-    if (work_group > T3_BS_THREADS && c->variant != T3DES_CU_VARIANT_SPTABLE) return T3DES_CU_ERR_ARG;
+    if (work_group > T3_BS_THREADS && c->variant != T3DES_CU_VARIANT_SPTABLE && c->variant != T3DES_CU_VARIANT_AUTO)
+        return T3DES_CU_ERR_ARG;
     c->chunk_blocks = chunk_blocks;
     c->work_group = work_group;
     return T3DES_CU_OK;

@@ -57,7 +57,7 @@ struct Opts {
     bool pkcs7 = false, check_parity = false, strict_keys = false;
     std::size_t chunk_blocks = 131072, work_group = 0;  // work_group: CTA threads, 0 = kernel default
     unsigned workers = 0;
-    std::string backend = "cuda", variant = "bitslice";
+    std::string backend = "cuda", variant = "auto";
     int device = 0;
     // bench
     std::string sweep = "chunk", format = "csv", out, mode = "device";
@@ -128,7 +128,8 @@ Opts parse(int argc, char** argv) {
         throw UsageError("unexpected argument: " + pos[0]);
     }
     if (o.backend != "cuda") throw UsageError("--backend must be cuda (the reference's CPU backends are not in this engine)");
-    if (o.variant != "bitslice" && o.variant != "sptable") throw UsageError("--variant must be bitslice|sptable");
+    if (o.variant != "auto" && o.variant != "bitslice" && o.variant != "sptable")
+        throw UsageError("--variant must be auto|bitslice|sptable");
     if (o.cmd == "bench") {
         if (o.sweep != "workers" && o.sweep != "chunk" && o.sweep != "workgroup")
             throw UsageError("--sweep must be workers|chunk|workgroup");
@@ -170,7 +171,9 @@ t3des::DispatchConfig make_config(const Opts& o) {
         if (const char* env = std::getenv("T3DES_WORKERS")) cfg.workers = static_cast<unsigned>(std::strtoul(env, nullptr, 10));
     cfg.backend = t3des::Backend::Cuda;
     cfg.device = o.device;
-    cfg.variant = o.variant == "sptable" ? T3DES_CU_VARIANT_SPTABLE : T3DES_CU_VARIANT_BITSLICE;
+    cfg.variant = o.variant == "sptable"    ? T3DES_CU_VARIANT_SPTABLE
+                  : o.variant == "bitslice" ? T3DES_CU_VARIANT_BITSLICE
+                                            : T3DES_CU_VARIANT_AUTO;
     return cfg;
 }
 
@@ -349,8 +352,7 @@ int run_bench(const Opts& o) {
                 cudaMalloc(&dout, bytes);
                 cudaMemcpy(din, payload.data(), bytes, cudaMemcpyHostToDevice);
                 rc = t3des_cu_set_schedule(c, sub48);
-                if (!rc) rc = t3des_cu_set_variant(c, o.variant == "sptable" ? T3DES_CU_VARIANT_SPTABLE
-                                                                           : T3DES_CU_VARIANT_BITSLICE);
+                if (!rc) rc = t3des_cu_set_variant(c, make_config(o).variant);
                 if (!rc) rc = t3des_cu_set_launch(c, r.chunk, static_cast<int>(r.wg));
                 cudaEvent_t e0, e1;
                 cudaEventCreate(&e0);
@@ -441,7 +443,7 @@ int run_bench(const Opts& o) {
 const char* kUsage =
     "usage: t3des_b200 <encrypt|decrypt> [--key HEX | --key-file F] [input|-] [output|-] [--pkcs7]\n"
     "                  [--check-parity] [--strict-keys] [--chunk-blocks N] [--work-group N]\n"
-    "                  [--workers N] [--backend cuda] [--variant bitslice|sptable] [--device D]\n"
+    "                  [--workers N] [--backend cuda] [--variant auto|bitslice|sptable] [--device D]\n"
     "       t3des_b200 verify [--device D]\n"
     "       t3des_b200 bench [--sweep workers|chunk|workgroup] [--values a,b,...] [--payload-mb M]\n"
     "                  [--seed S] [--reps R] [--format csv|markdown] [--out F] [--mode device|host]\n";

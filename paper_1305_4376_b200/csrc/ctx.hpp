@@ -21,7 +21,7 @@ struct t3des_cu_ctx {
     int bs_opt = T3_OPT_DEFAULT_VALUE;  // T3_OPT_* mask of the default bitsliced variant
     int sp_occ = 1;
     bool have_schedule = false;
-    int variant = T3DES_CU_VARIANT_BITSLICE;
+    int variant = T3DES_CU_VARIANT_AUTO;
     std::size_t chunk_blocks = 0;
     int work_group = 0;
     T3BsTable bs[2];

@@ -20,8 +20,8 @@ pytestmark = pytest.mark.gpu
 
 BENCH_KEY = "133457799BBCDFF10E329232EA6D0D737CA110454A1A6E57"
 KEYS = [BENCH_KEY, "0123456789ABCDEF23456789ABCDEF01", "0123456789ABCDEF"]
-VARIANTS = [N.VARIANT_BITSLICE, N.VARIANT_BITSLICE_ALU, N.VARIANT_BITSLICE_DFMA, N.VARIANT_BITSLICE_SHRFMA,
-            N.VARIANT_BITSLICE_LDG, N.VARIANT_SPTABLE]
+VARIANTS = [N.VARIANT_AUTO, N.VARIANT_BITSLICE, N.VARIANT_BITSLICE_ALU, N.VARIANT_BITSLICE_DFMA,
+            N.VARIANT_BITSLICE_SHRFMA, N.VARIANT_BITSLICE_LDG, N.VARIANT_SPTABLE]
 
 
 def dev(a: np.ndarray, pad: int = 0):
