@@ -77,6 +77,8 @@ static int g_budget = 40;  /* max gates (including the 6 inputs) */
 static int g_deep5 = 1;    /* enable the 2-gate search */
 static int g_deep5_depth = 1;  /* ... down to this recursion depth */
 static int g_gate_sel = 0;     /* internal gates tried as mux selectors at depth 0 */
+static int g_pair_tries = 0;   /* pair splits LUT3(a, b, g) tried per node */
+static int g_pair_depth = 0;   /* ... down to this depth */
 static uint64_t g_rng = 88172645463325252ull;
 
 static uint64_t rnd(void) {
@@ -223,10 +225,53 @@ static int build(circ_t* st, tt_t T, tt_t M, int avail, int depth) {
         if (g >= 0) return g;
     }
     if (st->n + 3 > g_budget) return -1;
-    /* split on a selector input */
     circ_t best;
     int best_g = -1;
     best.n = 1 << 30;
+    /* pair split: T = LUT3(a, b, g) for existing a, b; g only has to match T
+     * (up to a per-cell polarity) on the (a,b)-cells where T is not constant */
+    if (depth <= g_pair_depth && g_pair_tries > 0) {
+        int n = st->n;
+        /* rank pairs by the number of care positions left for g */
+        int cand_a[64], cand_b[64], cand_c[64], nc = 0;
+        for (int t = 0; t < 4 * g_pair_tries && nc < 64; t++) {
+            int a = (int)(rnd() % (unsigned)n), b = (int)(rnd() % (unsigned)n);
+            if (a == b) continue;
+            tt_t A = st->tt[a], B = st->tt[b];
+            tt_t Q[4] = {~A & ~B & M, ~A & B & M, A & ~B & M, A & B & M};
+            int care = 0;
+            for (int q = 0; q < 4; q++) {
+                tt_t t1 = Q[q] & T;
+                if (t1 != 0 && t1 != Q[q]) care += __builtin_popcountll(Q[q]);
+            }
+            cand_a[nc] = a; cand_b[nc] = b; cand_c[nc] = care; nc++;
+        }
+        for (int k = 0; k < g_pair_tries && nc > 0; k++) {
+            int bi = 0;
+            for (int i = 1; i < nc; i++) if (cand_c[i] < cand_c[bi]) bi = i;
+            int a = cand_a[bi], b = cand_b[bi];
+            cand_c[bi] = 1 << 30;
+            tt_t A = st->tt[a], B = st->tt[b];
+            tt_t Q[4] = {~A & ~B & M, ~A & B & M, A & ~B & M, A & B & M};
+            tt_t gm = 0, gt = T;
+            for (int q = 0; q < 4; q++) {
+                tt_t t1 = Q[q] & T;
+                if (t1 != 0 && t1 != Q[q]) {
+                    gm |= Q[q];
+                    if (rnd() & 1) gt ^= Q[q];  /* free polarity per mixed cell */
+                }
+            }
+            if (gm == 0) continue;
+            circ_t c = *st;
+            int g = build(&c, gt, gm, avail, depth + 1);
+            if (g < 0 || c.n >= g_budget) continue;
+            uint8_t l;
+            if (!find_lut3(c.tt[a], c.tt[b], c.tt[g], T, M, &l)) continue;
+            int h = add_gate(&c, a, b, g, l);
+            if (c.n < best.n) { best = c; best_g = h; }
+        }
+    }
+    /* split on a selector input */
     int order[6 + MAXG], cnt = 0;
     for (int s = 0; s < 6; s++)
         if (avail & (1 << s)) order[cnt++] = s;
@@ -435,6 +480,8 @@ static void local_search(int box, long iters, const char* init, const char* out_
         g_deep5 = (rnd() & 1);
         g_deep5_depth = 1 + (int)(rnd() % 3);
         g_gate_sel = (int)(rnd() % 4);
+        g_pair_tries = (int)(rnd() % 4);
+        g_pair_depth = (int)(rnd() % 2);
         int ok = 1;
         const int swap = k == 2 && (rnd() & 1);
         for (int j = 0; j < k && ok; j++) {
@@ -499,6 +546,8 @@ int main(int argc, char** argv) {
         g_deep5 = (rnd() & 3) != 0;
         g_deep5_depth = 1 + (int)(rnd() % 3);
         g_gate_sel = (int)(rnd() % 4);
+        g_pair_tries = (int)(rnd() % 4);
+        g_pair_depth = (int)(rnd() % 2);
         int ord[4] = {0, 1, 2, 3};
         for (int i = 3; i > 0; i--) {
             int j = (int)(rnd() % (unsigned)(i + 1));
