@@ -187,6 +187,18 @@ def run_reference_impl(args, rank: int, world: int) -> None:
     print(json.dumps(line), flush=True)
 
 
+def executed_alu_ops_per_block() -> float:
+    """ALU-pipe lane-ops per block of the shipped bitsliced kernel: 48 rounds x
+    (S-box LOP3 total + 32 Feistel/key LOP3) / 32 blocks per slice, plus four
+    32x32 slice transposes (64 PRMT + 96 LOP3 + 48 SHF each) / 32 blocks.  The
+    16 E-duplicate corrections and the whitening run on the FMA pipe."""
+    import re
+
+    with open(os.path.join(ROOT, "paper_1305_4376_b200", "csrc", "generated", "bitslice_rounds.cuh")) as f:
+        total = int(re.search(r"T3_SBOX_LOP3_TOTAL (\d+)", f.read()).group(1))
+    return round(48 * (total + 32) / 32 + 4 * (64 + 96 + 48) / 32, 2)
+
+
 def pcie_bidir(host, nbytes: int) -> float:
     """Raw pinned-host <-> device copy rate with both directions in flight
     (the ceiling of the e2e number), GB/s each way."""
@@ -207,7 +219,34 @@ def pcie_bidir(host, nbytes: int) -> float:
     return round(2 * nbytes / (time.perf_counter() - t0) / 1e9, 2)
 
 
-def extra_configs(e, orc, t3, N, torch, np) -> dict:
+def nist_kat_ok(t3) -> bool:
+    pt = bytes.fromhex("54686520717566636B2062726F776E20666F78206A756D70")
+    ct = bytearray(len(pt))
+    t3.encrypt_batch(pt, ct, t3.triple_schedule(t3.parse_hex_key("0123456789ABCDEF23456789ABCDEF01456789ABCDEF0123")))
+    return ct.hex().upper() == "A826FD8CE53B855FCCE21C8112256FE668D5C05DD9B6B900"
+
+
+def cross_check(e, N, torch, src, dst, nblocks, stream, variant) -> bool:
+    """Bitsliced output vs the SP-table kernel (an independent implementation)
+    on every 4096th block, and the decrypt round trip, on the bench payload."""
+    idx = torch.arange(0, nblocks, max(1, nblocks // 4096), device="cuda")
+    sample_in = src.view(torch.int64)[idx].contiguous()
+    e.set_variant(variant)
+    e.ecb_device(0, src.data_ptr(), dst.data_ptr(), 8 * nblocks, stream)
+    torch.cuda.synchronize()
+    got = dst.view(torch.int64)[idx].contiguous()
+    ref = torch.empty_like(sample_in)
+    e.set_variant(N.VARIANT_SPTABLE)
+    e.ecb_device(0, sample_in.data_ptr(), ref.data_ptr(), 8 * ref.numel(), stream)
+    e.set_variant(variant)
+    torch.cuda.synchronize()
+    cs_in = e.checksum(src.data_ptr(), 0, nblocks, stream)
+    e.ecb_device(1, dst.data_ptr(), dst.data_ptr(), 8 * nblocks, stream)
+    ok = bool(torch.equal(got, ref)) and e.checksum(dst.data_ptr(), 0, nblocks, stream) == cs_in
+    return ok
+
+
+def extra_configs(e, t3, N, torch, np) -> dict:
     """The other BASELINE.json configs, each checked before it is timed:
     [0] 1 MiB encrypt+decrypt, 3 distinct keys, NIST KAT;
     [2] 4 GiB decrypt, device-resident and end to end;
@@ -220,16 +259,21 @@ def extra_configs(e, orc, t3, N, torch, np) -> dict:
     ct = bytearray(len(pt))
     t3.encrypt_batch(pt, ct, t3.triple_schedule(t3.parse_hex_key(kat_key)))
     kat_ok = ct.hex().upper() == "A826FD8CE53B855FCCE21C8112256FE668D5C05DD9B6B900"
-    x = orc.payload(1 << 20)
-    s = orc.schedule_hex(BENCH_KEY)
-    e.set_variant(N.VARIANT_AUTO)  # the product default: <= 1 MiB runs the low-latency SP-table kernel
-    d = torch.from_numpy(x).cuda()
+    nb1 = (1 << 20) // 8
+    d = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+    e.fill_splitmix(d.data_ptr(), 0, nb1, SEED, stream)
     y = torch.empty_like(d)
     z = torch.empty_like(d)
-    e.ecb_device(0, d.data_ptr(), y.data_ptr(), x.nbytes, stream)
-    e.ecb_device(1, y.data_ptr(), z.data_ptr(), x.nbytes, stream)
+    e.set_variant(N.VARIANT_BITSLICE)
+    e.ecb_device(0, d.data_ptr(), z.data_ptr(), 1 << 20, stream)
+    e.set_variant(N.VARIANT_AUTO)  # the product default: <= 1 MiB runs the low-latency SP-table kernel
+    e.ecb_device(0, d.data_ptr(), y.data_ptr(), 1 << 20, stream)
     torch.cuda.synchronize()
-    ok = bool(np.array_equal(y.cpu().numpy(), orc.ecb(x, s, 0))) and bool(torch.equal(z, d))
+    ok = bool(torch.equal(y, z))  # both kernels agree
+    e.ecb_device(1, y.data_ptr(), z.data_ptr(), 1 << 20, stream)
+    torch.cuda.synchronize()
+    ok = ok and bool(torch.equal(z, d))  # and decrypt inverts encrypt
+    x = d
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for _ in range(3):
         e.ecb_device(0, d.data_ptr(), y.data_ptr(), x.nbytes, stream)
@@ -241,7 +285,7 @@ def extra_configs(e, orc, t3, N, torch, np) -> dict:
     torch.cuda.synchronize()
     us = ev0.elapsed_time(ev1) * 1e3 / 50
     out["c0_1MiB_enc_dec"] = {"us_per_enc_plus_dec": round(us, 2), "GBps_enc_plus_dec": round(2 * x.nbytes / us / 1e3, 2),
-                              "bit_exact_vs_oracle": ok, "nist_sp800_67_kat": kat_ok,
+                              "kernels_agree_and_round_trip": ok, "nist_sp800_67_kat": kat_ok,
                               "note": "latency bound (1 MiB = 128 warp tiles); variant AUTO runs the SP-table "
                                       "kernel at this size"}
     del d, y, z
@@ -395,17 +439,13 @@ def main() -> None:
         e.fill_splitmix(src.data_ptr(), first_block, nblocks, SEED, sp)
     torch.cuda.synchronize()
 
-    # sampled correctness gate before timing (bit-exact vs the CPU oracle)
-    from tests.oracle_util import Oracle
+    # correctness gate before timing, without the CPU oracle (that is test
+    # infrastructure; tests/ compare the kernels against it bit for bit):
+    # the NIST SP 800-67 vector through the engine, the bitsliced output vs
+    # the independent SP-table kernel on a sample, and decrypt(encrypt(x)) == x
     import numpy as np
 
-    orc = Oracle.load()
-    e.ecb_device(0, src.data_ptr(), dst.data_ptr(), nbytes, sp)
-    torch.cuda.synchronize()
-    idx = torch.arange(0, nblocks, max(1, nblocks // 4096), device="cuda")
-    got = dst.view(torch.int64)[idx].cpu().numpy().view(np.uint8)
-    inp = src.view(torch.int64)[idx].cpu().numpy().view(np.uint8)
-    parity_ok = bool(np.array_equal(got, orc.ecb(inp, orc.schedule_hex(BENCH_KEY), 0)))
+    parity_ok = nist_kat_ok(t3) and cross_check(e, N, torch, src, dst, nblocks, sp, VARIANTS[args.variant])
 
     for _ in range(args.warmup):
         e.ecb_device(0, src.data_ptr(), dst.data_ptr(), nbytes, sp)
@@ -431,6 +471,7 @@ def main() -> None:
     fmax = float(peaks.get("sm_max_mhz", 1965.0))
     peak_tlops = sms * ALU_LANES_PER_CLK_PER_SM * fmax * 1e6 / 1e12
     per_gpu_bps = nblocks / (ms_step * 1e-3)
+    alu_ops = executed_alu_ops_per_block()
     achieved = per_gpu_bps * W_ALG / 1e12
     traffic = args.traffic_bytes
     if traffic is None:
@@ -449,6 +490,11 @@ def main() -> None:
         "frac_at_run_clock": (round(achieved / (sms * 64 * clocks["sm_mhz"] * 1e6 / 1e12), 4)
                               if clocks.get("sm_mhz") else None),
         "w_alg_lane_ops_per_block": W_ALG,
+        # what the shipped kernel actually issues to the ALU pipe per block
+        # (static SASS-level count: S-box LOP3 + Feistel LOP3 per round, plus
+        # the slice transposes), and the utilisation that implies
+        "executed_alu_lane_ops_per_block": alu_ops,
+        "alu_pipe_frac": round(per_gpu_bps * alu_ops / (peak_tlops * 1e12), 4),
         "hbm": {"achieved_gbs": round(per_gpu_bps * 16 / 1e9, 2), "peak_gbs": hbm_peak,
                 "frac": round(per_gpu_bps * 16 / 1e9 / hbm_peak, 4), "bytes_per_block": 16},
     }
@@ -459,7 +505,8 @@ def main() -> None:
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": workload_config(args, world),
         "roofline": roofline, "clocks": clocks, "gpu_launches": int(launches),
-        "parity_sampled_vs_oracle": parity_ok,
+        "self_check": {"ok": parity_ok, "how": "NIST SP 800-67 KAT via the engine; bitsliced == SP-table kernel "
+                       "on a 1/4096 sample; decrypt(encrypt(x)) == x checksum"},
     }
 
     # the other variants (north star: bitsliced vs SP-table, ncu picks)
@@ -508,7 +555,7 @@ def main() -> None:
         line["e2e"] = None
 
     if not args.no_extra_configs and world == 1:
-        line["configs_measured"] = extra_configs(e, orc, t3, N, torch, np)
+        line["configs_measured"] = extra_configs(e, t3, N, torch, np)
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         g, cores, kind, desc = cpu_reference_arm()
