@@ -406,6 +406,149 @@ static void resub(circ_t* c, int* outs, const tt_t* tgt) {
     (void)tgt;
 }
 
+/* ---- cone rewriting: |MFFC(h)| >= 3 replaced by 2 new gates ------------ */
+/* Mark the maximum fanout-free cone of h (gates that die if h dies). */
+static int mffc(const circ_t* c, const int* outs, int h, int* in_cone) {
+    int fo[MAXG];
+    fanouts(c, outs, fo);
+    memset(in_cone, 0, sizeof(int) * MAXG);
+    in_cone[h] = 1;
+    int size = 1;
+    for (int g = h; g >= 6; g--) {
+        if (!in_cone[g]) continue;
+        for (int k = 0; k < 3; k++) {
+            int x = c->in[g][k];
+            if (x < 6 || in_cone[x]) continue;
+            /* x dies if all its fanouts are inside the cone */
+            int uses_in = 0;
+            for (int y = x + 1; y < c->n; y++)
+                if (in_cone[y]) uses_in += (c->in[y][0] == x) + (c->in[y][1] == x) + (c->in[y][2] == x);
+            int is_out = 0;
+            for (int o = 0; o < 4; o++) is_out |= outs[o] == x;
+            if (!is_out && uses_in == fo[x]) { in_cone[x] = 1; size++; }
+        }
+    }
+    return size;
+}
+
+/* 2-gate search restricted to allowed signals (LUT3(LUT3(a,b,c), x, y)), exact
+ * on the full table; on success appends the two gates and returns the top. */
+static int search5_allowed(circ_t* st, tt_t T, const int* allowed) {
+    int n = st->n;
+    int idx[MAXG], m = 0;
+    for (int i = 0; i < n; i++) if (allowed[i]) idx[m++] = i;
+    for (int ia = 0; ia < m; ia++)
+        for (int ib = ia + 1; ib < m; ib++)
+            for (int ic = ib + 1; ic < m; ic++) {
+                int a = idx[ia], b = idx[ib], c = idx[ic];
+                tt_t mt[8];
+                for (int q = 0; q < 8; q++)
+                    mt[q] = ((q & 4) ? st->tt[a] : ~st->tt[a]) & ((q & 2) ? st->tt[b] : ~st->tt[b]) &
+                            ((q & 1) ? st->tt[c] : ~st->tt[c]);
+                for (int ix = 0; ix < m; ix++)
+                    for (int iy = ix + 1; iy < m; iy++) {
+                        int x = idx[ix], y = idx[iy];
+                        tt_t X = st->tt[x], Y = st->tt[y];
+                        tt_t Q[4] = {~X & ~Y, ~X & Y, X & ~Y, X & Y};
+                        int ok = 1;
+                        for (int i = 0; i < 12; i++) { uf_p[i] = i; uf_x[i] = 0; }
+                        for (int q = 0; q < 4 && ok; q++) {
+                            tt_t t1 = Q[q] & T;
+                            if (t1 == 0 || t1 == Q[q]) continue;
+                            for (int u = 0; u < 8; u++) {
+                                tt_t cell = mt[u] & Q[q];
+                                if (!cell) continue;
+                                tt_t v1 = cell & T;
+                                int v;
+                                if (v1 == 0) v = 0;
+                                else if (v1 == cell) v = 1;
+                                else { ok = 0; break; }
+                                if (!uf_union(u, 8 + q, v)) { ok = 0; break; }
+                            }
+                        }
+                        if (!ok) continue;
+                        uint8_t hl = 0;
+                        for (int u = 0; u < 8; u++) {
+                            int p;
+                            uf_find(u, &p);
+                            if (p) hl |= (uint8_t)(1u << u);
+                        }
+                        tt_t H = lut_eval(hl, st->tt[a], st->tt[b], st->tt[c]);
+                        uint8_t ol;
+                        if (!find_lut3(H, X, Y, T, ~0ull, &ol)) continue;
+                        int h = add_gate(st, a, b, c, hl);
+                        return add_gate(st, h, x, y, ol);
+                    }
+            }
+    return -1;
+}
+
+/* Try to shrink the circuit by cone rewriting; returns 1 if it improved. */
+static int rewrite2(circ_t* c, int* outs) {
+    for (int h = c->n - 1; h >= 6; h--) {
+        int cone[MAXG];
+        int sz = mffc(c, outs, h, cone);
+        if (sz < 3) continue;
+        /* allowed: not in the cone and not in h's transitive fanout */
+        int allowed[MAXG], tfo[MAXG];
+        memset(tfo, 0, sizeof tfo);
+        tfo[h] = 1;
+        for (int g = h + 1; g < c->n; g++)
+            for (int k = 0; k < 3; k++) if (tfo[c->in[g][k]]) tfo[g] = 1;
+        for (int g = 0; g < c->n; g++) allowed[g] = !cone[g] && !tfo[g];
+        circ_t t = *c;
+        int top = search5_allowed(&t, c->tt[h], allowed);
+        if (top < 0) continue;
+        /* redirect every consumer of h to top; gates appended at the end, so
+         * move h's consumers after them by rebuilding in topological order */
+        circ_t r;
+        r.n = 6;
+        for (int i = 0; i < 6; i++) r.tt[i] = c->tt[i];
+        int map[MAXG];
+        for (int i = 0; i < 6; i++) map[i] = i;
+        /* emit: old gates (except cone) that do not depend on h, then the 2
+         * new gates, then the rest */
+        for (int g = 6; g < c->n; g++) map[g] = -1;
+        int order_pass;
+        for (order_pass = 0; order_pass < 2; order_pass++) {
+            for (int g = 6; g < c->n; g++) {
+                if (cone[g] || map[g] >= 0) continue;
+                if ((order_pass == 0) == (tfo[g] != 0)) continue;
+                int a = c->in[g][0], b = c->in[g][1], cc = c->in[g][2];
+                int ma = a == h ? map[h] : map[a], mb = b == h ? map[h] : map[b], mc = cc == h ? map[h] : map[cc];
+                if (ma < 0 || mb < 0 || mc < 0) { order_pass = 9; break; }
+                map[g] = add_gate(&r, ma, mb, mc, c->lut[g]);
+            }
+            if (order_pass == 0) {
+                int g1 = t.n - 2, g2 = t.n - 1;
+                int a = t.in[g1][0], b = t.in[g1][1], cc = t.in[g1][2];
+                if (map[a] < 0 || map[b] < 0 || map[cc] < 0) { order_pass = 9; break; }
+                int n1 = add_gate(&r, map[a], map[b], map[cc], t.lut[g1]);
+                int x = t.in[g2][1], y = t.in[g2][2];
+                if (map[x] < 0 || map[y] < 0) { order_pass = 9; break; }
+                map[h] = add_gate(&r, n1, map[x], map[y], t.lut[g2]);
+            }
+        }
+        if (order_pass > 2) continue;
+        int nouts[4];
+        int okk = 1;
+        for (int o = 0; o < 4; o++) {
+            nouts[o] = map[outs[o]];
+            if (nouts[o] < 0) okk = 0;
+        }
+        if (!okk) continue;
+        for (int o = 0; o < 4; o++) {
+            tt_t d = r.tt[nouts[o]] ^ c->tt[outs[o]];
+            if (d != 0 && d != ~0ull) okk = 0;
+        }
+        if (!okk || r.n >= c->n) continue;
+        *c = r;
+        memcpy(outs, nouts, sizeof nouts);
+        return 1;
+    }
+    return 0;
+}
+
 static tt_t out_tt(int box, int bit) {
     tt_t t = 0;
     for (int p = 0; p < 64; p++) {
@@ -463,6 +606,10 @@ static void local_search(int box, long iters, const char* init, const char* out_
         exit(2);
     }
     fprintf(stderr, "box %d start: %d gates\n", box, best.n - 6);
+    resub(&best, best_out, tgt);
+    while (rewrite2(&best, best_out)) resub(&best, best_out, tgt);
+    fprintf(stderr, "box %d after rewriting: %d gates\n", box, best.n - 6);
+    dump(out_path, box, &best, best_out, tgt);
     int record = best.n;
     for (long it = 0; it < iters; it++) {
         circ_t c = best;
@@ -492,6 +639,7 @@ static void local_search(int box, long iters, const char* init, const char* out_
         }
         if (!ok) continue;
         resub(&c, outs, tgt);
+        while (rewrite2(&c, outs)) resub(&c, outs, tgt);
         int valid = 1;
         for (int o = 0; o < 4; o++) {
             tt_t d = c.tt[outs[o]] ^ tgt[o];
@@ -561,6 +709,7 @@ int main(int argc, char** argv) {
         }
         if (!ok) continue;
         resub(&c, outs, tgt);
+        while (rewrite2(&c, outs)) resub(&c, outs, tgt);
         if (c.n < best.n) {
             best = c;
             memcpy(best_out, outs, sizeof outs);
