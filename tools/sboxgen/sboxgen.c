@@ -549,6 +549,83 @@ static int rewrite2(circ_t* c, int* outs) {
     return 0;
 }
 
+/* General cone resynthesis: rebuild tt[h] from the signals outside its
+ * fanout-free cone (and outside its transitive fanout) with the randomized
+ * builder under a budget of |cone| - 1 new gates; splice on success. */
+static int rewrite_cone(circ_t* c, int* outs, int tries) {
+    for (int h = c->n - 1; h >= 6; h--) {
+        int cone[MAXG];
+        int k = mffc(c, outs, h, cone);
+        if (k < 2) continue;
+        int tfo[MAXG];
+        memset(tfo, 0, sizeof tfo);
+        tfo[h] = 1;
+        for (int g = h + 1; g < c->n; g++)
+            for (int j = 0; j < 3; j++) if (tfo[c->in[g][j]]) tfo[g] = 1;
+        /* sub-circuit of allowed signals */
+        circ_t sub;
+        int sub2orig[MAXG];
+        sub.n = 6;
+        for (int i = 0; i < 6; i++) { sub.tt[i] = c->tt[i]; sub2orig[i] = i; }
+        for (int g = 6; g < c->n; g++)
+            if (!cone[g] && !tfo[g]) {
+                sub.tt[sub.n] = c->tt[g];
+                sub.in[sub.n][0] = sub.in[sub.n][1] = sub.in[sub.n][2] = -1;
+                sub.lut[sub.n] = 0;
+                sub2orig[sub.n++] = g;
+            }
+        const int base = sub.n;
+        for (int t = 0; t < tries; t++) {
+            circ_t w = sub;
+            g_budget = base + k - 1;
+            int top = build(&w, c->tt[h], ~0ull, 0x3F, 0);
+            if (top < 0 || top < base) continue; /* top < base: an existing signal matches (resub handles) */
+            if (w.n - base >= k) continue;
+            /* splice: keep non-cone, non-TFO gates; then the new gates; then TFO */
+            circ_t r;
+            r.n = 6;
+            for (int i = 0; i < 6; i++) r.tt[i] = c->tt[i];
+            int map[MAXG];
+            for (int g = 0; g < 6; g++) map[g] = g;
+            for (int g = 6; g < c->n; g++) map[g] = -1;
+            for (int g = 6; g < c->n; g++)
+                if (!cone[g] && !tfo[g])
+                    map[g] = add_gate(&r, map[c->in[g][0]], map[c->in[g][1]], map[c->in[g][2]], c->lut[g]);
+            int wmap[MAXG];
+            for (int i = 0; i < base; i++) wmap[i] = map[sub2orig[i]];
+            for (int i = base; i < w.n; i++)
+                wmap[i] = add_gate(&r, wmap[w.in[i][0]], wmap[w.in[i][1]], wmap[w.in[i][2]], w.lut[i]);
+            map[h] = wmap[top];
+            int bad = 0;
+            for (int g = h + 1; g < c->n && !bad; g++) {
+                if (!tfo[g]) continue;
+                int a = map[c->in[g][0]], b = map[c->in[g][1]], cc = map[c->in[g][2]];
+                if (a < 0 || b < 0 || cc < 0) { bad = 1; break; }
+                /* an inverted replacement is absorbed by re-deriving the LUT */
+                uint8_t l;
+                if (!find_lut3(r.tt[a], r.tt[b], r.tt[cc], c->tt[g], ~0ull, &l)) { bad = 1; break; }
+                map[g] = add_gate(&r, a, b, cc, l);
+            }
+            if (bad) continue;
+            int nouts[4];
+            for (int o = 0; o < 4; o++) {
+                nouts[o] = map[outs[o]];
+                if (nouts[o] < 0) bad = 1;
+                else {
+                    tt_t d = r.tt[nouts[o]] ^ c->tt[outs[o]];
+                    if (d != 0 && d != ~0ull) bad = 1;
+                }
+            }
+            if (bad || r.n >= c->n) continue;
+            *c = r;
+            memcpy(outs, nouts, sizeof nouts);
+            sweep(c, outs);
+            return 1;
+        }
+    }
+    return 0;
+}
+
 static tt_t out_tt(int box, int bit) {
     tt_t t = 0;
     for (int p = 0; p < 64; p++) {
@@ -608,6 +685,15 @@ static void local_search(int box, long iters, const char* init, const char* out_
     fprintf(stderr, "box %d start: %d gates\n", box, best.n - 6);
     resub(&best, best_out, tgt);
     while (rewrite2(&best, best_out)) resub(&best, best_out, tgt);
+    {
+        int saved = g_budget;
+        for (int pass = 0; pass < 3; pass++)
+            while (rewrite_cone(&best, best_out, 6)) {
+                resub(&best, best_out, tgt);
+                while (rewrite2(&best, best_out)) resub(&best, best_out, tgt);
+            }
+        g_budget = saved;
+    }
     fprintf(stderr, "box %d after rewriting: %d gates\n", box, best.n - 6);
     dump(out_path, box, &best, best_out, tgt);
     int record = best.n;
