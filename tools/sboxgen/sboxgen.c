@@ -775,8 +775,10 @@ int main(int argc, char** argv) {
             c.in[i][0] = c.in[i][1] = c.in[i][2] = -1;
             c.lut[i] = 0;
         }
-        g_budget = (best.n < (1 << 30) ? best.n - 1 : cap);
-        if (g_budget > cap) g_budget = cap;
+        /* allow a few gates of slack: the rewriting passes below often
+         * shrink a near-miss circuit below the record */
+        g_budget = (best.n < (1 << 30) ? best.n - 1 + 3 : cap);
+        if (g_budget > cap + 3) g_budget = cap + 3;
         g_deep5 = (rnd() & 3) != 0;
         g_deep5_depth = 1 + (int)(rnd() % 3);
         g_gate_sel = (int)(rnd() % 4);
@@ -796,6 +798,14 @@ int main(int argc, char** argv) {
         if (!ok) continue;
         resub(&c, outs, tgt);
         while (rewrite2(&c, outs)) resub(&c, outs, tgt);
+        {
+            const int saved = g_budget;
+            while (rewrite_cone(&c, outs, 4)) {
+                resub(&c, outs, tgt);
+                while (rewrite2(&c, outs)) resub(&c, outs, tgt);
+            }
+            g_budget = saved;
+        }
         if (c.n < best.n) {
             best = c;
             memcpy(best_out, outs, sizeof outs);
