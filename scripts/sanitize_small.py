@@ -21,13 +21,17 @@ for v in variants:
     e.set_variant(v)
     for n in (1, 33, 1024, 1025, 8 * 1024 * 40 + 17, 300_000):
         for pad in (0, 8):
-            buf = torch.randint(0, 255, (8 * n + pad + 16,), dtype=torch.uint8, device="cuda")
+            buf = torch.randint(0, 255, (8 * n + pad + 64,), dtype=torch.uint8, device="cuda")
             src = buf[pad:pad + 8 * n]
-            dst = torch.empty(8 * n + 16, dtype=torch.uint8, device="cuda")[:8 * n]
+            out = torch.full((8 * n + 128,), 0xA5, dtype=torch.uint8, device="cuda")
+            dst = out[64 + pad:64 + pad + 8 * n]
+            guard = out.clone()
             e.ecb_device(0, src.data_ptr(), dst.data_ptr(), 8 * n, s)
             e.ecb_device(1, dst.data_ptr(), dst.data_ptr(), 8 * n, s)
             torch.cuda.synchronize()
             assert torch.equal(dst, src), (v, n, pad)
+            assert torch.equal(out[:64 + pad], guard[:64 + pad]) and torch.equal(out[64 + pad + 8 * n:],
+                                                                                guard[64 + pad + 8 * n:]), (v, n, pad)
 x = bytes(range(256)) * 4000
 out = io.BytesIO()
 t3.encrypt_stream(io.BytesIO(x), out, ts, t3.DispatchConfig(chunk_blocks=1000), t3.PaddingMode.PKCS7)

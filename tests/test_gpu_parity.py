@@ -297,3 +297,26 @@ def test_64gib_sharding_invariance_on_one_device(eng, oracle):
         eng.ecb_device(1, buf.data_ptr(), buf.data_ptr(), 8 * n, st)  # back to plaintext
         assert eng.checksum(buf.data_ptr(), 0, n, st) == cs_plain
     assert len(set(sums.values())) == 1, sums
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_no_writes_outside_the_batch(eng, oracle, variant):
+    """Sentinel bytes before and after the output range survive every
+    variant, tail and alignment (compute-sanitizer is closed on this pool)."""
+    ts = t3.triple_schedule(t3.parse_hex_key(BENCH_KEY))
+    s = oracle.schedule_hex(BENCH_KEY)
+    eng.set_schedule(ts)
+    eng.set_variant(variant)
+    eng.set_launch(0, 0)
+    st = torch.cuda.current_stream().cuda_stream
+    for n in (1, 31, 1025, 8 * 1024 * 5 + 3):
+        for pad in (0, 8):
+            x = np.random.default_rng(n + pad).integers(0, 256, 8 * n, dtype=np.uint8)
+            src = dev(x, pad)
+            out = torch.full((8 * n + 256,), 0x5A, dtype=torch.uint8, device="cuda")
+            dst = out[128 + pad: 128 + pad + 8 * n]
+            eng.ecb_device(0, src.data_ptr(), dst.data_ptr(), 8 * n, st)
+            torch.cuda.synchronize()
+            o = out.cpu().numpy()
+            assert (o[:128 + pad] == 0x5A).all() and (o[128 + pad + 8 * n:] == 0x5A).all(), (n, pad)
+            assert np.array_equal(o[128 + pad: 128 + pad + 8 * n], oracle.ecb(x, s, 0))
