@@ -129,6 +129,16 @@ int t3des_cu_set_pipeline(t3des_cu_ctx* ctx, size_t chunk_bytes, int streams);
 int t3des_cu_ecb_multi(const int* devices, int ndev, const uint64_t sub48[48], int direction,
                        const uint8_t* in, uint8_t* out, size_t len);
 
+/* Device-resident multi-GPU (NVLink 5 / NVSwitch): din/dout
+ * live on `home_device`; shard g (t3des_cu_shard_range) is copied to
+ * devices[g] with cudaMemcpyPeerAsync, transformed there and copied back.
+ * A shard whose device is the home device is transformed in place of
+ * din -> dout without copies unless flags & T3DES_CU_MULTI_STAGE_ALL.
+ * Synchronous.  Peer access is enabled where the topology allows it. */
+#define T3DES_CU_MULTI_STAGE_ALL 1
+int t3des_cu_ecb_multi_device(const int* devices, int ndev, const uint64_t sub48[48], int direction,
+                              int home_device, const void* din, void* dout, size_t len, int flags);
+
 /* The block range device `g` of `ndev` owns in t3des_cu_ecb_multi (and in
  * bench.py's torchrun ranks): [first, first + count), boundaries at
  * floor(g*N/ndev) rounded down to 1024-block tiles; the last shard ends at N. */

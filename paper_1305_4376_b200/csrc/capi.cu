@@ -410,6 +410,60 @@ int t3des_cu_ecb_multi(const int* devices, int ndev, const std::uint64_t sub48[4
     return T3DES_CU_OK;
 }
 
+int t3des_cu_ecb_multi_device(const int* devices, int ndev, const std::uint64_t sub48[48], int dir,
+                              int home, const void* din, void* dout, std::size_t len, int flags) {
+    if (!devices || ndev <= 0 || !sub48 || (dir != 0 && dir != 1)) return T3DES_CU_ERR_ARG;
+    if (len % 8) return T3DES_CU_ERR_LENGTH;
+    if (len && (!din || !dout)) return T3DES_CU_ERR_ARG;
+    if (partial_overlap(din, dout, len)) return T3DES_CU_ERR_OVERLAP;
+    if (!len) return T3DES_CU_OK;
+    const std::uint64_t nblocks = len / 8;
+    const auto* in = static_cast<const std::uint8_t*>(din);
+    auto* out = static_cast<std::uint8_t*>(dout);
+    std::vector<t3des_cu_ctx*> ctx(ndev, nullptr);
+    std::vector<std::uint8_t*> stage(ndev, nullptr);
+    int rc = T3DES_CU_OK;
+    // issue every shard asynchronously on its device's stream, then wait
+    for (int g = 0; g < ndev && !rc; ++g) {
+        std::uint64_t first = 0, count = 0;
+        t3des_cu_shard_range(nblocks, ndev, g, &first, &count);
+        if (!count) continue;
+        rc = t3des_cu_create(devices[g], &ctx[g]);
+        if (!rc) rc = t3des_cu_set_schedule(ctx[g], sub48);
+        if (rc) break;
+        DeviceScope scope(devices[g]);
+        cudaStream_t s = ctx[g]->st[0];
+        const std::size_t bytes = 8 * count;
+        if (devices[g] == home && !(flags & T3DES_CU_MULTI_STAGE_ALL)) {
+            rc = run_device(ctx[g], dir, in + 8 * first, out + 8 * first, count, s);
+            continue;
+        }
+        if (devices[g] != home) {
+            int can = 0;
+            if (cudaDeviceCanAccessPeer(&can, devices[g], home) == cudaSuccess && can) {
+                const cudaError_t e = cudaDeviceEnablePeerAccess(home, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) rc = T3DES_CU_ERR_CUDA;
+                (void)cudaGetLastError();
+            }
+        }
+        if (!rc && cudaMalloc(&stage[g], bytes) != cudaSuccess) rc = T3DES_CU_ERR_CUDA;
+        if (!rc && cudaMemcpyPeerAsync(stage[g], devices[g], in + 8 * first, home, bytes, s) != cudaSuccess)
+            rc = T3DES_CU_ERR_CUDA;
+        if (!rc) rc = run_device(ctx[g], dir, stage[g], stage[g], count, s);
+        if (!rc && cudaMemcpyPeerAsync(out + 8 * first, home, stage[g], devices[g], bytes, s) != cudaSuccess)
+            rc = T3DES_CU_ERR_CUDA;
+    }
+    for (int g = 0; g < ndev; ++g) {
+        if (!ctx[g]) continue;
+        DeviceScope scope(devices[g]);
+        if (cudaStreamSynchronize(ctx[g]->st[0]) != cudaSuccess && !rc) rc = T3DES_CU_ERR_CUDA;
+        if (stage[g]) cudaFree(stage[g]);
+        t3des_cu_destroy(ctx[g]);
+    }
+    (void)cudaGetLastError();
+    return rc;
+}
+
 int t3des_cu_host_alloc(std::size_t bytes, void** out) {
     if (!out) return T3DES_CU_ERR_ARG;
     *out = nullptr;

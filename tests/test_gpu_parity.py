@@ -320,3 +320,25 @@ def test_no_writes_outside_the_batch(eng, oracle, variant):
             o = out.cpu().numpy()
             assert (o[:128 + pad] == 0x5A).all() and (o[128 + pad + 8 * n:] == 0x5A).all(), (n, pad)
             assert np.array_equal(o[128 + pad: 128 + pad + 8 * n], oracle.ecb(x, s, 0))
+
+
+def test_multi_device_resident_scatter_gather(oracle):
+    """t3des_cu_ecb_multi_device: data resident on the home GPU, shards sent
+    to the devices with cudaMemcpyPeerAsync and back.  With one GPU the
+    staging path (STAGE_ALL) runs every copy as a device-local peer copy."""
+    ngpu = torch.cuda.device_count()
+    devs = list(range(ngpu)) if ngpu > 1 else [0, 0, 0]
+    s = oracle.schedule_hex(BENCH_KEY)
+    n = 3 * 1024 * 9 + 5
+    x = oracle.payload(8 * n)
+    src = dev(x)
+    arr = (ctypes.c_int * len(devs))(*devs)
+    for flags in (0, 1):
+        dst = torch.empty_like(src)
+        rc = N.lib().t3des_cu_ecb_multi_device(arr, len(devs), s, 0, 0, src.data_ptr(), dst.data_ptr(), x.nbytes,
+                                               flags)
+        assert rc == 0
+        assert np.array_equal(host(dst), oracle.ecb(x, s, 0)), flags
+    # in place, decrypt
+    rc = N.lib().t3des_cu_ecb_multi_device(arr, len(devs), s, 1, 0, dst.data_ptr(), dst.data_ptr(), x.nbytes, 1)
+    assert rc == 0 and np.array_equal(host(dst), x)
