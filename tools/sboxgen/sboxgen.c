@@ -650,6 +650,7 @@ static void dump(const char* path, int box, const circ_t* c, const int* outs, co
 }
 
 /* ---- local search: rip up outputs and rebuild them -------------------- */
+static int rewrite_cone(circ_t* c, int* outs, int tries);
 static int load_circuit(const char* path, circ_t* c, int* outs) {
     FILE* f = fopen(path, "r");
     if (!f) return 0;
@@ -709,7 +710,7 @@ static void local_search(int box, long iters, const char* init, const char* out_
         which[1] = (which[0] + 1 + (int)(rnd() % 3)) % 4;
         for (int j = 0; j < k; j++) outs[which[j]] = 0;
         sweep(&c, outs);
-        g_budget = best.n;  /* accept equal cost */
+        g_budget = best.n + 2;  /* allow near misses; cone resynthesis may shrink them */
         g_deep5 = (rnd() & 1);
         g_deep5_depth = 1 + (int)(rnd() % 3);
         g_gate_sel = (int)(rnd() % 4);
@@ -726,6 +727,14 @@ static void local_search(int box, long iters, const char* init, const char* out_
         if (!ok) continue;
         resub(&c, outs, tgt);
         while (rewrite2(&c, outs)) resub(&c, outs, tgt);
+        if (c.n <= best.n + 2) {  /* near misses get the cone resynthesis too */
+            const int saved = g_budget;
+            while (rewrite_cone(&c, outs, 3)) {
+                resub(&c, outs, tgt);
+                while (rewrite2(&c, outs)) resub(&c, outs, tgt);
+            }
+            g_budget = saved;
+        }
         int valid = 1;
         for (int o = 0; o < 4; o++) {
             tt_t d = c.tt[outs[o]] ^ tgt[o];
