@@ -21,7 +21,9 @@
 #include "t3des_core.cuh"
 
 #define T3_BS_THREADS 128
-#define T3_BS_MIN_CTAS 4
+#ifndef T3_BS_MIN_CTAS
+#define T3_BS_MIN_CTAS 4  // resident CTAs per SM the register budget is sized for
+#endif
 #define T3_SP_THREADS 256
 #define T3_TILE_BLOCKS 1024  // blocks per warp tile (32 lanes x 32 blocks)
 #ifndef T3_OPT_DEFAULT
