@@ -54,7 +54,9 @@ int launch_bitslice(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8
                     std::uint64_t nblocks, cudaStream_t s) {
     const std::uint64_t full = nblocks / T3_TILE_BLOCKS;
     const bool tail = (nblocks % T3_TILE_BLOCKS) != 0;
-    const int threads = c->work_group > 0 ? c->work_group : T3_BS_THREADS;
+    // work_group is a CTA-size hint; the bitsliced kernels are built for at
+    // most T3_BS_THREADS threads (AUTO may pass a larger SP-table size)
+    const int threads = c->work_group > 0 ? std::min(c->work_group, T3_BS_THREADS) : T3_BS_THREADS;
     if (full) {
         const std::uint64_t warps_per_cta = std::uint64_t(threads) / 32;
         std::uint64_t grid = (full + warps_per_cta - 1) / warps_per_cta;

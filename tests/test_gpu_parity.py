@@ -342,3 +342,13 @@ def test_multi_device_resident_scatter_gather(oracle):
     # in place, decrypt
     rc = N.lib().t3des_cu_ecb_multi_device(arr, len(devs), s, 1, 0, dst.data_ptr(), dst.data_ptr(), x.nbytes, 1)
     assert rc == 0 and np.array_equal(host(dst), x)
+
+
+def test_auto_variant_with_large_work_group(eng, oracle):
+    """AUTO + a 256-thread work group: small launches use it on the SP-table
+    kernel, large ones clamp it to the bitsliced kernel's 128 threads."""
+    ts = t3.triple_schedule(t3.parse_hex_key(BENCH_KEY))
+    s = oracle.schedule_hex(BENCH_KEY)
+    for n in (1000, 300_000):
+        x = np.random.default_rng(n).integers(0, 256, 8 * n, dtype=np.uint8)
+        assert np.array_equal(run(eng, ts, x, 0, N.VARIANT_AUTO, wg=256), oracle.ecb(x, s, 0)), n
