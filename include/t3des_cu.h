@@ -118,8 +118,9 @@ int t3des_cu_ecb_device(t3des_cu_ctx* ctx, int direction, const void* din, void*
 int t3des_cu_ecb_host(t3des_cu_ctx* ctx, int direction, const uint8_t* in, uint8_t* out,
                       size_t len);
 
-/* Host-path pipeline shape: bytes per stage (multiple of 8; default 32 MiB)
- * and number of streams/staging buffers (1..8; default 3). */
+/* Host-path pipeline shape: bytes per stage (multiple of 8) and number of
+ * streams/staging buffers (1..8).  Default: 3 streams, stage size adapted
+ * to each batch (about len/8, clamped to 8..32 MiB). */
 int t3des_cu_set_pipeline(t3des_cu_ctx* ctx, size_t chunk_bytes, int streams);
 
 /* Host buffers sharded by contiguous block ranges (multiples of 1024

@@ -339,7 +339,15 @@ int t3des_cu_ecb_host(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uin
     if (rc) return rc;
     if (!len) return T3DES_CU_OK;
     DeviceScope scope(c->device);
-    const std::size_t chunk = std::min(len, c->pipe_chunk);
+    // Stage size: as set, or adapted to the batch — about 8 stages, between
+    // 8 and 32 MiB (scripts/e2e_size_sweep.py: 32-64 MiB batches gain ~10-30%
+    // from 8 MiB stages, >= 256 MiB batches prefer 32 MiB), whole tiles.
+    std::size_t chunk = c->pipe_chunk;
+    if (!c->pipe_explicit) {
+        chunk = std::min(chunk, std::max(std::size_t(8) << 20, len / 8));
+        chunk -= chunk % (8 * T3_TILE_BLOCKS);
+    }
+    chunk = std::min(len, chunk);
     const int ns = c->pipe_streams;
     rc = t3b::ensure_staging(c, chunk, ns);
     if (rc) return rc;
@@ -365,6 +373,7 @@ int t3des_cu_set_pipeline(t3des_cu_ctx* c, std::size_t chunk_bytes, int streams)
         return T3DES_CU_ERR_ARG;
     c->pipe_chunk = chunk_bytes;
     c->pipe_streams = streams;
+    c->pipe_explicit = true;
     return T3DES_CU_OK;
 }
 

@@ -32,8 +32,9 @@ struct t3des_cu_ctx {
     cudaStream_t st[kMaxStreams] = {};
     std::uint8_t* buf[kMaxStreams] = {};
     std::size_t buf_bytes = 0;
-    std::size_t pipe_chunk = std::size_t(32) << 20;  // bytes per pipeline stage
+    std::size_t pipe_chunk = std::size_t(32) << 20;  // bytes per pipeline stage (upper bound)
     int pipe_streams = 3;
+    bool pipe_explicit = false;  // set by t3des_cu_set_pipeline; else stages adapt to the batch
     std::uint64_t launches = 0;
 };
 
