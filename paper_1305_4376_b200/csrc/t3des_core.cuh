@@ -156,6 +156,10 @@ T3_FI void t3_xor_table(uint32_t (&h)[32], const KP k, const KP s) {
     for (int q = 0; q < 32; ++q) h[q] = (OPT & T3_OPT_WFMA) ? t3_dfix<T3_OPT_DFMA>(h[q], k[q], s[q]) : (h[q] ^ k[q]);
 }
 
+#ifndef T3_BODY_ROUNDS
+#define T3_BODY_ROUNDS 2  // rounds per loop iteration (2 or 4)
+#endif
+
 // All 48 rounds (3 passes of 16) on halves A (initial L) and B (initial R).
 // The pass-final half swaps of the reference (tdes.cpp:151-159) are role
 // renamings: pass 2 runs with the roles of A and B exchanged.
@@ -169,6 +173,30 @@ T3_FI void t3_cipher(uint32_t (&A)[32], uint32_t (&B)[32], const KP w) {
     // One loop of 23 bodies with the two single rounds (and the
     // re-whitenings) behind uniform branches keeps 4 rounds of code instead
     // of 6 (instruction-cache footprint).
+#if T3_BODY_ROUNDS == 4
+    // 4-round body: [AB AB]x4, B, [AB AB]x3, [AB], A, [AB AB]x4
+    auto body2 = [&](int r) {
+        t3_round<OPT>(A, B, w + T3_TAB_ROUND + r * T3_ROUND_WORDS);
+        t3_round<OPT>(B, A, w + T3_TAB_ROUND + (r + 1) * T3_ROUND_WORDS);
+    };
+    int r = 0;
+#pragma unroll 1
+    for (int it = 0; it < 11; ++it) {
+        body2(r);
+        body2(r + 2);
+        r += 4;
+        if (it == 3) {  // after round 15
+            t3_xor_table<OPT>(A, w + T3_TAB_RW1, w + T3_TAB_WS + 64);
+            t3_round<OPT>(B, A, w + T3_TAB_ROUND + 16 * T3_ROUND_WORDS);
+            r = 17;
+        } else if (it == 6) {  // rounds 17..28 done: 29, 30, then 31 = A <- B
+            body2(29);
+            t3_round<OPT>(A, B, w + T3_TAB_ROUND + 31 * T3_ROUND_WORDS);
+            t3_xor_table<OPT>(B, w + T3_TAB_RW2, w + T3_TAB_WS + 96);
+            r = 32;
+        }
+    }
+#else
     int r = 0;
 #pragma unroll 1
     for (int it = 0; it < 23; ++it) {
@@ -185,6 +213,7 @@ T3_FI void t3_cipher(uint32_t (&A)[32], uint32_t (&B)[32], const KP w) {
             r = 32;
         }
     }
+#endif
     // B is never read after round 48, so its final whitening is 0 (checked
     // on the host); only A is un-whitened.
     t3_xor_table<OPT>(A, w + T3_TAB_POST, w + T3_TAB_WS + 128);
