@@ -403,11 +403,20 @@ def main() -> None:
     import paper_1305_4376_b200 as t3
     from paper_1305_4376_b200 import _native as N
 
-    torch.cuda.set_device(local)
+    # one rank per GPU; T3DES_BENCH_DIST_BACKEND=gloo lets the multi-rank
+    # logic run with several ranks on one GPU (ranks never wait on each
+    # other's kernels; NCCL refuses two ranks on one device)
+    backend = os.environ.get("T3DES_BENCH_DIST_BACKEND", "nccl")
+    device = local % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(device)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device))
+        else:
+            dist.init_process_group(backend)
 
     def barrier():
+        torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -415,11 +424,11 @@ def main() -> None:
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    e = t3.Engine(local)
+    e = t3.Engine(device)
     ts = t3.triple_schedule(t3.parse_hex_key(BENCH_KEY))
     e.set_schedule(ts)
     VARIANTS = {"bitslice": N.VARIANT_BITSLICE, "bitslice_alu": N.VARIANT_BITSLICE_ALU,
@@ -452,7 +461,7 @@ def main() -> None:
     barrier()
     l0 = e.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(device) as clk:
         barrier()
         ev0.record(stream)
         for _ in range(args.steps):
@@ -467,7 +476,7 @@ def main() -> None:
     clocks = clk.summary()
 
     peaks = measured_peaks()
-    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    sms = torch.cuda.get_device_properties(device).multi_processor_count
     fmax = float(peaks.get("sm_max_mhz", 1965.0))
     peak_tlops = sms * ALU_LANES_PER_CLK_PER_SM * fmax * 1e6 / 1e12
     per_gpu_bps = nblocks / (ms_step * 1e-3)
