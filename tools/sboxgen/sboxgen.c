@@ -194,6 +194,57 @@ static int search5(circ_t* st, tt_t T, tt_t M) {
     return -1;
 }
 
+/* 3-gate step, guided: T = LUT3(h1, h2, y) with h1 = majority-LUT of a
+ * random triple (the LUT agreeing with T on most care positions), h2 a new
+ * LUT3 of existing signals, y existing.  Returns the top gate or -1. */
+static int g_search7 = 0;  /* candidate h1 per node (0 = off) */
+static int search7_guided(circ_t* st, tt_t T, tt_t M) {
+    int n = st->n;
+    for (int cand = 0; cand < g_search7; cand++) {
+        int a = (int)(rnd() % (unsigned)n), b = (int)(rnd() % (unsigned)n), c = (int)(rnd() % (unsigned)n);
+        if (a == b || b == c || a == c) continue;
+        uint8_t l = 0;
+        for (int m = 0; m < 8; m++) {
+            tt_t P = M & ((m & 4) ? st->tt[a] : ~st->tt[a]) & ((m & 2) ? st->tt[b] : ~st->tt[b]) &
+                     ((m & 1) ? st->tt[c] : ~st->tt[c]);
+            if (2 * __builtin_popcountll(P & T) > __builtin_popcountll(P)) l |= (uint8_t)(1u << m);
+        }
+        tt_t H1 = lut_eval(l, st->tt[a], st->tt[b], st->tt[c]);
+        /* outer inputs: H1 and y (existing); h2 = LUT3(d,e,f) new */
+        for (int y = 0; y < n; y++) {
+            tt_t Y = st->tt[y];
+            tt_t Q[4] = {~H1 & ~Y & M, ~H1 & Y & M, H1 & ~Y & M, H1 & Y & M};
+            int mixed = 0;
+            tt_t need = 0;
+            for (int q = 0; q < 4; q++) {
+                tt_t t1 = Q[q] & T;
+                if (t1 != 0 && t1 != Q[q]) { mixed |= 1 << q; need |= Q[q]; }
+            }
+            if (!mixed) continue; /* 2 gates would do; search5 covers that */
+            /* h2 must equal T ^ pol_q on each mixed cell: try the 2^k-1 polarities */
+            int cells[4], k = 0;
+            for (int q = 0; q < 4; q++) if (mixed & (1 << q)) cells[k++] = q;
+            for (int pol = 0; pol < (1 << (k - 1)); pol++) {
+                tt_t target = T;
+                for (int i = 1; i < k; i++) if (pol & (1 << (i - 1))) target ^= Q[cells[i]];
+                for (int d = 0; d < n; d++)
+                    for (int e = d + 1; e < n; e++)
+                        for (int f = e + 1; f < n; f++) {
+                            uint8_t l2;
+                            if (!find_lut3(st->tt[d], st->tt[e], st->tt[f], target, need, &l2)) continue;
+                            tt_t H2 = lut_eval(l2, st->tt[d], st->tt[e], st->tt[f]);
+                            uint8_t l3;
+                            if (!find_lut3(H1, H2, Y, T, M, &l3)) continue;
+                            int g1 = add_gate(st, a, b, c, l);
+                            int g2 = add_gate(st, d, e, f, l2);
+                            return add_gate(st, g1, g2, y, l3);
+                        }
+            }
+        }
+    }
+    return -1;
+}
+
 /* Returns gate index, or -1 if budget exhausted. */
 static int build(circ_t* st, tt_t T, tt_t M, int avail, int depth) {
     if (M == 0) return 0;
@@ -225,6 +276,11 @@ static int build(circ_t* st, tt_t T, tt_t M, int avail, int depth) {
         if (g >= 0) return g;
     }
     if (st->n + 3 > g_budget) return -1;
+    if (g_search7 && depth <= 1) {
+        circ_t c = *st;
+        int g = search7_guided(&c, T, M);
+        if (g >= 0) { *st = c; return g; }
+    }
     circ_t best;
     int best_g = -1;
     best.n = 1 << 30;
@@ -716,6 +772,7 @@ static void local_search(int box, long iters, const char* init, const char* out_
         g_gate_sel = (int)(rnd() % 4);
         g_pair_tries = (int)(rnd() % 4);
         g_pair_depth = (int)(rnd() % 2);
+        g_search7 = (rnd() & 1) ? (int)(rnd() % 24) : 0;
         int ok = 1;
         const int swap = k == 2 && (rnd() & 1);
         for (int j = 0; j < k && ok; j++) {
@@ -793,6 +850,7 @@ int main(int argc, char** argv) {
         g_gate_sel = (int)(rnd() % 4);
         g_pair_tries = (int)(rnd() % 4);
         g_pair_depth = (int)(rnd() % 2);
+        g_search7 = (rnd() & 1) ? (int)(rnd() % 24) : 0;
         int ord[4] = {0, 1, 2, 3};
         for (int i = 3; i > 0; i--) {
             int j = (int)(rnd() % (unsigned)(i + 1));
