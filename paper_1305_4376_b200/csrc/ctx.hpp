@@ -36,6 +36,8 @@ struct t3des_cu_ctx {
     int pipe_streams = 3;
     bool pipe_explicit = false;  // set by t3des_cu_set_pipeline; else stages adapt to the batch
     std::uint64_t launches = 0;
+    cudaStream_t tail_st = nullptr;             // side stream for the partial tile (AUTO)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 namespace t3b {
