@@ -1,14 +1,17 @@
 // sm_100a kernels of the B200 3DES-ECB engine.
 //
-//   t3_bs_kernel  bitsliced 3DES (primary): one warp owns a tile of 1024
-//                 blocks (8 KiB), each thread 32 blocks held as 64 slice
-//                 words; loads/stores are coalesced 128-bit (or 64-bit when
-//                 the buffers are only 8-byte aligned), the rounds are pure
-//                 lop3 on the integer pipe with key/whitening constants read
-//                 from constant bank 0 (__grid_constant__ table, LDCU).
-//   t3_sp_kernel  SP-table variant (measured alternative): one block per
-//                 thread per step, the 8 fused S/P tables replicated per lane
-//                 in shared memory (64 KiB, bank = lane: conflict-free).
+//   t3_bs_tma_kernel  bitsliced 3DES, the shipped kernel: one warp owns a
+//                 tile of 1024 blocks (8 KiB), each thread 32 blocks held as
+//                 64 slice words; the warp's next tile streams into shared
+//                 memory by TMA (cp.async.bulk) while it computes; the rounds
+//                 are LOP3 circuits on the integer pipe with key/whitening
+//                 constants from constant bank 0 (__grid_constant__ table).
+//   t3_bs_kernel  the same cipher with direct 128-bit (or 64-bit, for
+//                 8-byte-aligned buffers) loads, and the predicated tail tile.
+//   t3_sp_kernel  SP-table variant (measured alternative; AUTO uses it for
+//                 small launches and partial tiles): one block per thread per
+//                 step, the 8 fused S/P tables replicated per lane in shared
+//                 memory (64 KiB, bank = lane: conflict-free).
 //   helpers       splitmix payload generator, order-sensitive checksum.
 //
 // Replaces the reference's Threaded backend inner loop
@@ -29,7 +32,6 @@
 #ifndef T3_OPT_DEFAULT
 #define T3_OPT_DEFAULT T3_OPT_DFMA  // for the LDG/tail kernels; the TMA kernel's mask is per context
 #endif
-
 
 // ---- bitsliced kernel --------------------------------------------------
 // VEC = 4: lane t of the warp loads blocks (64j + 2t, 64j + 2t + 1), j < 16,
