@@ -23,7 +23,9 @@
 
 #include "t3des_core.cuh"
 
-#define T3_BS_THREADS 128
+#ifndef T3_BS_THREADS
+#define T3_BS_THREADS 128  // CTA size of the bitsliced kernels
+#endif
 #ifndef T3_BS_MIN_CTAS
 #define T3_BS_MIN_CTAS 4  // resident CTAs per SM the register budget is sized for
 #endif
