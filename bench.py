@@ -322,6 +322,34 @@ def extra_configs(e, t3, N, torch, np) -> dict:
                               "note": "device: 5 decrypts of the 4 GiB ciphertext, CUDA events; "
                                       "e2e: t3des_cu_ecb_host pinned in -> pinned out incl. H2D/D2H"}
     del host
+    # configs[4] edge case: K1 = K2 = K3 (option 3) is single DES; the engine
+    # detects the collapsed EDE and runs 16 rounds instead of 48
+    e3 = t3.Engine(e.device)
+    e3.set_schedule(t3.triple_schedule(t3.parse_hex_key("0123456789ABCDEF")))
+    n1 = (1 << 30) // 8
+    b1 = torch.empty(8 * n1, dtype=torch.uint8, device="cuda")
+    b2 = torch.empty_like(b1)
+    e3.fill_splitmix(b1.data_ptr(), 0, n1, SEED, stream)
+    kat = bytearray(8)
+    t3.encrypt_batch(bytes.fromhex("4E6F772069732074"), kat, t3.triple_schedule(t3.parse_hex_key("0123456789ABCDEF")))
+    for _ in range(3):
+        e3.ecb_device(0, b1.data_ptr(), b2.data_ptr(), 8 * n1, stream)
+    torch.cuda.synchronize()
+    ev0.record()
+    for _ in range(5):
+        e3.ecb_device(0, b1.data_ptr(), b2.data_ptr(), 8 * n1, stream)
+    ev1.record()
+    torch.cuda.synchronize()
+    ms3 = ev0.elapsed_time(ev1) / 5
+    e3.ecb_device(1, b2.data_ptr(), b2.data_ptr(), 8 * n1, stream)
+    torch.cuda.synchronize()
+    out["c4_option3_1GiB_encrypt"] = {"device_GBps": round(8 * n1 / ms3 / 1e6, 2),
+                                      "kat_3FA40E8A984D4815": kat.hex().upper() == "3FA40E8A984D4815",
+                                      "round_trip_ok": bool(torch.equal(b1, b2)),
+                                      "note": "K1 = K2 = K3: EDE collapses to single DES, 16 rounds"}
+    del b1, b2
+    e3.close()
+    torch.cuda.empty_cache()
     # configs[3]: 64 GiB in block-range shards; on one device the G shards
     # run back to back (the torchrun bench runs them on G GPUs)
     from paper_1305_4376_b200.sharding import shard_range

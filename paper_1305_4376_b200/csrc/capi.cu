@@ -94,7 +94,11 @@ int launch_bitslice(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8
                         : c->variant == T3DES_CU_VARIANT_BITSLICE_ALU ? 0
                         : c->variant == T3DES_CU_VARIANT_BITSLICE_DFMA ? T3_OPT_DFMA
                                                                        : T3_OPT_SHRFMA;
-        if (tma) {
+        if (tma && c->rounds == 16 && opt == T3_OPT_DEFAULT_VALUE) {
+            // collapsed EDE (K1 = K2 or K2 = K3): single DES, a third of the work
+            t3_bs_tma_kernel<T3_OPT_DEFAULT_VALUE, 16>
+                <<<unsigned(grid), threads, 0, s>>>(in, out, full, c->bs16[dir]);
+        } else if (tma) {
             switch (opt) {
 #define T3_TMA_CASE(O)                                                                                  \
     case O:                                                                                             \
@@ -132,8 +136,10 @@ int launch_sptable(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8_
     const int threads = c->work_group > 0 ? c->work_group : T3_SP_THREADS;
     std::uint64_t grid = (nblocks + threads - 1) / threads;
     grid = std::min<std::uint64_t>(grid, std::uint64_t(c->sms) * std::uint64_t(c->sp_occ));
+    const bool single = c->rounds == 16;
     t3_sp_kernel<<<unsigned(std::max<std::uint64_t>(grid, 1)), threads, kSpSmemBytes, s>>>(
-        reinterpret_cast<const uint2*>(in), reinterpret_cast<uint2*>(out), nblocks, c->d_sp, c->sp[dir]);
+        reinterpret_cast<const uint2*>(in), reinterpret_cast<uint2*>(out), nblocks, c->d_sp, single ? 1 : 3,
+        single ? c->sp16[dir] : c->sp[dir]);
     T3_CK(cudaGetLastError());
     ++c->launches;
     return T3DES_CU_OK;
@@ -318,6 +324,7 @@ int t3des_cu_destroy(t3des_cu_ctx* c) {
 
 int t3des_cu_set_schedule(t3des_cu_ctx* c, const std::uint64_t sub48[48]) {
     if (!c || !sub48) return T3DES_CU_ERR_ARG;
+    c->rounds = 48;
     for (int dir = 0; dir < 2; ++dir) {
         std::uint64_t seq[48];
         t3b::key_sequence(sub48, dir == T3DES_CU_DECRYPT, seq);
@@ -325,6 +332,14 @@ int t3des_cu_set_schedule(t3des_cu_ctx* c, const std::uint64_t sub48[48]) {
         t3b::SpKeys k;
         t3b::build_sp_keys(seq, k);
         std::memcpy(c->sp[dir].k, k.k, sizeof k.k);
+        // K1 = K2 or K2 = K3: the EDE collapses to single DES (16 rounds)
+        std::uint64_t seq16[48] = {};
+        if (t3b::collapsed_sequence(sub48, dir == T3DES_CU_DECRYPT, seq16) == 16) {
+            c->rounds = 16;
+            t3b::build_bitslice_table(seq16, c->bs16[dir], 16);
+            t3b::build_sp_keys(seq16, k);
+            std::memcpy(c->sp16[dir].k, k.k, sizeof k.k);
+        }
     }
     c->have_schedule = true;
     return T3DES_CU_OK;

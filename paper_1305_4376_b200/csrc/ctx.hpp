@@ -24,8 +24,11 @@ struct t3des_cu_ctx {
     int variant = T3DES_CU_VARIANT_AUTO;
     std::size_t chunk_blocks = 0;
     int work_group = 0;
-    T3BsTable bs[2];
+    T3BsTable bs[2];       // 48-round tables, encrypt / decrypt
     T3SpKeyParam sp[2];
+    int rounds = 48;       // 16 when the schedule collapses to single DES
+    T3BsTable bs16[2];     // collapsed (16-round) tables
+    T3SpKeyParam sp16[2];
     std::uint32_t* d_sp = nullptr;  // 8x64 fused S/P table (2 KiB)
     unsigned long long* d_acc = nullptr;
     static constexpr int kMaxStreams = 8;

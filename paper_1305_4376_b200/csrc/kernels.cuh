@@ -116,7 +116,7 @@ __device__ __forceinline__ void t3_mbar_wait(uint32_t bar, uint32_t parity) {
         : "memory");
 }
 
-template <int OPT>
+template <int OPT, int ROUNDS = 48>
 __global__ void __launch_bounds__(T3_BS_THREADS, T3_BS_MIN_CTAS)
 t3_bs_tma_kernel(const uint8_t* in, uint8_t* out, uint64_t ntiles, const __grid_constant__ T3BsTable tab) {
     __shared__ __align__(128) uint4 slot[T3_BS_THREADS / 32][T3_TILE_BLOCKS / 2];
@@ -153,7 +153,7 @@ t3_bs_tma_kernel(const uint8_t* in, uint8_t* out, uint64_t ntiles, const __grid_
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             t3_tma_fetch(sdst, in + next * (T3_TILE_BLOCKS * 8), T3_TILE_BLOCKS * 8, sbar);
         }
-        t3_tile32<OPT>(lo, hi, tab.w);
+        t3_tile32<OPT, ROUNDS>(lo, hi, tab.w);
         uint4* dst = reinterpret_cast<uint4*>(out + tile * (T3_TILE_BLOCKS * 8)) + lane;
 #pragma unroll
         for (int j = 0; j < 16; ++j)
@@ -184,7 +184,7 @@ __device__ __forceinline__ uint32_t t3_sp_f(uint32_t r, const uint32_t* k, const
 
 __global__ void __launch_bounds__(T3_SP_THREADS)
 t3_sp_kernel(const uint2* in, uint2* out, uint64_t nblocks, const uint32_t* __restrict__ sp_global,
-             const __grid_constant__ T3SpKeyParam kp) {
+             int passes, const __grid_constant__ T3SpKeyParam kp) {
     extern __shared__ uint32_t t3_sp_smem[];
     for (int w = threadIdx.x; w < 8 * 64 * 32; w += blockDim.x) t3_sp_smem[w] = sp_global[w >> 5];
     __syncthreads();
@@ -205,15 +205,17 @@ t3_sp_kernel(const uint2* in, uint2* out, uint64_t nblocks, const uint32_t* __re
             x ^= t3_sp_f(y, kp.k[t], smem_lane);
             y ^= t3_sp_f(x, kp.k[t + 1], smem_lane);
         }
+        if (passes == 3) {  // 1 = collapsed EDE (single DES)
 #pragma unroll 1
-        for (int t = 16; t < 32; t += 2) {
-            y ^= t3_sp_f(x, kp.k[t], smem_lane);
-            x ^= t3_sp_f(y, kp.k[t + 1], smem_lane);
-        }
+            for (int t = 16; t < 32; t += 2) {
+                y ^= t3_sp_f(x, kp.k[t], smem_lane);
+                x ^= t3_sp_f(y, kp.k[t + 1], smem_lane);
+            }
 #pragma unroll 1
-        for (int t = 32; t < 48; t += 2) {
-            x ^= t3_sp_f(y, kp.k[t], smem_lane);
-            y ^= t3_sp_f(x, kp.k[t + 1], smem_lane);
+            for (int t = 32; t < 48; t += 2) {
+                x ^= t3_sp_f(y, kp.k[t], smem_lane);
+                y ^= t3_sp_f(x, kp.k[t + 1], smem_lane);
+            }
         }
         // preoutput = y || x, then FP = the IP swaps in reverse order.
         uint32_t hi = y, lo = x;

@@ -109,7 +109,7 @@ void key_sequence(const std::uint64_t sub48[48], bool decrypt, std::uint64_t seq
 // A half that is read as R in round t must be stored XORed with the round
 // key bit of each bit's primary E slot; this function tracks the stored
 // whitening of both halves and emits the constants that keep it so.
-void build_bitslice_table(const std::uint64_t seq[48], T3BsTable& tab) {
+void build_bitslice_table(const std::uint64_t seq[48], T3BsTable& tab, int nrounds) {
     std::memset(&tab, 0, sizeof tab);
     auto l_role = [](int t) -> int {  // 0 = A, 1 = B
         const int pass = t / 16, loc = t % 16;
@@ -121,7 +121,7 @@ void build_bitslice_table(const std::uint64_t seq[48], T3BsTable& tab) {
     // primary key bits of the next round reading it, unless it is written
     // again first (then 0).
     auto target_after = [&](int half, int t, std::uint32_t out[32]) {
-        for (int t2 = t + 1; t2 < 48; ++t2) {
+        for (int t2 = t + 1; t2 < nrounds; ++t2) {
             if (l_role(t2) == half) break;  // overwritten before any read
             for (int q = 0; q < 32; ++q) out[q] = prim(t2, q);
             return;
@@ -133,7 +133,7 @@ void build_bitslice_table(const std::uint64_t seq[48], T3BsTable& tab) {
         target_after(h, -1, wh[h]);
         for (int q = 0; q < 32; ++q) tab.w[T3_TAB_PRE + 32 * h + q] = wh[h][q];
     }
-    for (int t = 0; t < 48; ++t) {
+    for (int t = 0; t < nrounds; ++t) {
         const int lh = l_role(t), rh = 1 - lh;
         if (t == 16 || t == 32) {
             // The R half was already read in round t-1 with that round's
@@ -171,6 +171,18 @@ void build_bitslice_table(const std::uint64_t seq[48], T3BsTable& tab) {
     for (int i = 0; i < 32; ++i) tab.w[T3_TAB_WS + 64 + i] = tab.w[T3_TAB_RW1 + i] | 1u;
     for (int i = 0; i < 32; ++i) tab.w[T3_TAB_WS + 96 + i] = tab.w[T3_TAB_RW2 + i] | 1u;
     for (int i = 0; i < 64; ++i) tab.w[T3_TAB_WS + 128 + i] = tab.w[T3_TAB_POST + i] | 1u;
+}
+
+int collapsed_sequence(const std::uint64_t sub48[48], bool decrypt, std::uint64_t seq16[16]) {
+    const std::uint64_t* p1 = sub48;
+    const std::uint64_t* p2 = sub48 + 16;
+    const std::uint64_t* p3 = sub48 + 32;
+    const std::uint64_t* single = nullptr;
+    if (std::memcmp(p1, p2, 16 * 8) == 0) single = p3;       // E_k3(D_k2(E_k1 x)) = E_k3 x
+    else if (std::memcmp(p2, p3, 16 * 8) == 0) single = p1;  // = E_k1 x
+    if (!single) return 48;
+    for (int t = 0; t < 16; ++t) seq16[t] = decrypt ? single[15 - t] : single[t];
+    return 16;
 }
 
 void build_sp_keys(const std::uint64_t seq[48], SpKeys& out) {

@@ -31,8 +31,14 @@ void triple_schedule(const std::uint64_t keys[3], std::uint64_t sub48[48]);
 void key_sequence(const std::uint64_t sub48[48], bool decrypt, std::uint64_t seq[48]);
 
 // Whitening/key-constant table of the bitsliced kernel for one execution
-// sequence (layout: T3_TAB_* in t3des_core.cuh).
-void build_bitslice_table(const std::uint64_t seq[48], T3BsTable& tab);
+// sequence of nrounds (48, or 16 for a collapsed schedule) round keys
+// (layout: T3_TAB_* in t3des_core.cuh).
+void build_bitslice_table(const std::uint64_t seq[48], T3BsTable& tab, int nrounds = 48);
+
+// EDE collapse: if k1 and k2 (or k2 and k3) have identical schedules, the
+// inner E/D pair is the identity and 3DES equals single DES under the
+// remaining key.  Writes that 16-key sequence and returns 16, else 48.
+int collapsed_sequence(const std::uint64_t sub48[48], bool decrypt, std::uint64_t seq16[16]);
 
 // Per-round 6-bit key chunks for the SP-table kernel: k6[r][i] is the key
 // input of S-box i in round r, shifted to bits 7..12 (pre-scaled as a byte

@@ -163,11 +163,20 @@ T3_FI void t3_xor_table(uint32_t (&h)[32], const KP k, const KP s) {
 // All 48 rounds (3 passes of 16) on halves A (initial L) and B (initial R).
 // The pass-final half swaps of the reference (tdes.cpp:151-159) are role
 // renamings: pass 2 runs with the roles of A and B exchanged.
-template <int OPT, class KP>
+template <int OPT, int ROUNDS = 48, class KP>
 T3_FI void t3_cipher(uint32_t (&A)[32], uint32_t (&B)[32], const KP w) {
     // A is written (round 1) before it is ever read, so its initial whitening
     // is 0 by construction (checked in build_bitslice_table); only B needs it.
     t3_xor_table<OPT>(B, w + T3_TAB_PRE + 32, w + T3_TAB_WS + 32);
+    if (ROUNDS == 16) {  // collapsed EDE (single DES): one pass, [A<-B, B<-A] x 8
+#pragma unroll 1
+        for (int r = 0; r < 16; r += 2) {
+            t3_round<OPT>(A, B, w + T3_TAB_ROUND + r * T3_ROUND_WORDS);
+            t3_round<OPT>(B, A, w + T3_TAB_ROUND + (r + 1) * T3_ROUND_WORDS);
+        }
+        t3_xor_table<OPT>(A, w + T3_TAB_POST, w + T3_TAB_WS + 128);
+        return;
+    }
     // Rounds as one shared 2-round body: pass 1 = [A<-B, B<-A] x 8; pass 2
     // (roles swapped) = B<-A, [A<-B, B<-A] x 7, A<-B; pass 3 = [A<-B, B<-A] x 8.
     // One loop of 23 bodies with the two single rounds (and the
@@ -221,13 +230,13 @@ T3_FI void t3_cipher(uint32_t (&A)[32], uint32_t (&B)[32], const KP w) {
 
 // One thread's 32 blocks: lo[m]/hi[m] are the little-endian words holding
 // bytes 0..3 / 4..7 of block m.  Transforms in place.
-template <int OPT, class KP>
+template <int OPT, int ROUNDS = 48, class KP>
 T3_FI void t3_tile32(uint32_t (&lo)[32], uint32_t (&hi)[32], const KP w) {
     t3_transpose32<OPT>(lo);
     t3_transpose32<OPT>(hi);
     uint32_t A[32] = T3_GATHER_A(lo, hi);
     uint32_t B[32] = T3_GATHER_B(lo, hi);
-    t3_cipher<OPT>(A, B, w);
+    t3_cipher<OPT, ROUNDS>(A, B, w);
     {
         uint32_t olo[32] = T3_SCATTER_LO(A, B);
         uint32_t ohi[32] = T3_SCATTER_HI(A, B);

@@ -137,4 +137,5 @@ def bs_host() -> ctypes.CDLL:
     lib = ctypes.CDLL(BS_HOST_SO)
     lib.bs_host_ecb.argtypes = [_vp, _vp, _sz, ctypes.POINTER(U64), ctypes.c_int]
     lib.bs_host_table.argtypes = [ctypes.POINTER(U64), ctypes.c_int, ctypes.POINTER(ctypes.c_uint32)]
+    lib.bs_host_ecb_collapse.argtypes = [_vp, _vp, _sz, ctypes.POINTER(U64), ctypes.c_int]
     return lib

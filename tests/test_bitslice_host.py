@@ -173,3 +173,23 @@ def test_ip_delta_swaps_match_fips(oracle):
         y, x = _dswap(y, x, 8, 0x00FF00FF)
         x, y = _dswap(x, y, 1, 0x55555555)
         assert (x << 32) | y == oracle.lib.oracle_permute(v, 64, 0)
+
+
+@pytest.mark.parametrize("keyhex,expect_rounds", [
+    ("0123456789ABCDEF", 16),                                           # option 3
+    ("0123456789ABCDEF0123456789ABCDEF456789ABCDEF0123", 16),           # K1 = K2
+    ("0123456789ABCDEF23456789ABCDEF0123456789ABCDEF01", 16),           # K2 = K3
+    ("0023456789ABCDEF0123456789ABCDEF456789ABCDEF0123", 16),           # K1, K2 differ only in parity
+    ("0123456789ABCDEF23456789ABCDEF01", 48),                           # option 2: no collapse
+    (KEYS[0], 48),
+])
+def test_collapsed_single_des_path(oracle, keyhex, expect_rounds):
+    """K1 = K2 or K2 = K3 (schedules equal): EDE = single DES, run as 16
+    bitsliced rounds; bit-exact with the full 48-round oracle."""
+    lib = bs_host()
+    s = oracle.schedule_hex(keyhex)
+    x = oracle.payload(8 * 32 * 12)
+    for d in (0, 1):
+        y = np.empty_like(x)
+        assert lib.bs_host_ecb_collapse(x.ctypes.data, y.ctypes.data, 32 * 12, s, d) == expect_rounds
+        assert np.array_equal(y, oracle.ecb(x, s, d, route=0)), (keyhex, d)

@@ -19,7 +19,8 @@ from tests.oracle_util import ROOT, checksum, sub48_from_hex_list  # noqa: E402
 pytestmark = pytest.mark.gpu
 
 BENCH_KEY = "133457799BBCDFF10E329232EA6D0D737CA110454A1A6E57"
-KEYS = [BENCH_KEY, "0123456789ABCDEF23456789ABCDEF01", "0123456789ABCDEF"]
+KEYS = [BENCH_KEY, "0123456789ABCDEF23456789ABCDEF01", "0123456789ABCDEF",
+        "0123456789ABCDEF0123456789ABCDEF456789ABCDEF0123"]  # opt 1, opt 2, opt 3, K1 = K2 (collapses)
 VARIANTS = [N.VARIANT_AUTO, N.VARIANT_BITSLICE, N.VARIANT_BITSLICE_ALU, N.VARIANT_BITSLICE_DFMA,
             N.VARIANT_BITSLICE_SHRFMA, N.VARIANT_BITSLICE_LDG, N.VARIANT_SPTABLE]
 
