@@ -140,3 +140,21 @@ int main() {
     subprocess.check_call(["/usr/bin/g++", "-std=c++20", "-I" + os.path.join(ROOT, "include"), str(src),
                            N.LIB_PATH, "-Wl,-rpath," + os.path.dirname(N.LIB_PATH), "-o", str(exe)])
     assert subprocess.run([str(exe)], capture_output=True, text=True).stdout.strip() == "ok"
+
+
+def test_pipeline_and_launch_argument_checks(engine_lib):
+    L = engine_lib
+    assert L.t3des_cu_set_pipeline(None, 1 << 20, 3) == N.ERR_ARG
+    assert L.t3des_cu_set_launch(None, 0, 0) == N.ERR_ARG
+    assert L.t3des_cu_set_variant(None, 0) == N.ERR_ARG
+    first, count = ctypes.c_uint64(), ctypes.c_uint64()
+    assert L.t3des_cu_shard_range(100, 0, 0, ctypes.byref(first), ctypes.byref(count)) == N.ERR_ARG
+    assert L.t3des_cu_shard_range(100, 2, 1, ctypes.byref(first), ctypes.byref(count)) == 0
+    assert (first.value, count.value) == (0, 100)  # 100 blocks < one tile: all in the last shard
+    rep = N.StreamReportC()
+    assert L.t3des_cu_stream_fd(None, 0, 0, 1, 16, 0, ctypes.byref(rep)) == N.ERR_ARG
+    assert L.t3des_cu_ecb_multi(None, 0, None, 0, None, None, 0) == N.ERR_ARG
+    devs = (ctypes.c_int * 1)(0)
+    sub = (ctypes.c_uint64 * 48)()
+    assert L.t3des_cu_ecb_multi(devs, 1, sub, 0, None, None, 12) == N.ERR_LENGTH
+    assert L.t3des_cu_ecb_multi_device(devs, 1, sub, 0, 0, None, None, 12, 0) == N.ERR_LENGTH

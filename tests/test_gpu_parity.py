@@ -353,3 +353,23 @@ def test_auto_variant_with_large_work_group(eng, oracle):
     for n in (1000, 300_000):
         x = np.random.default_rng(n).integers(0, 256, 8 * n, dtype=np.uint8)
         assert np.array_equal(run(eng, ts, x, 0, N.VARIANT_AUTO, wg=256), oracle.ecb(x, s, 0)), n
+
+
+def test_pipeline_shapes_give_identical_bytes(eng, oracle):
+    """t3des_cu_set_pipeline: any stage size / stream count (and the adaptive
+    default) produces the same bytes through the host path."""
+    ts = t3.triple_schedule(t3.parse_hex_key(BENCH_KEY))
+    s = oracle.schedule_hex(BENCH_KEY)
+    x = oracle.splitmix(0, (24 << 20) // 8 + 3, 5)
+    want = oracle.ecb(x, s, 0)
+    e = t3.Engine(0)
+    e.set_schedule(ts)
+    y = np.empty_like(x)
+    e.ecb_host(0, x.ctypes.data, y.ctypes.data, x.nbytes)  # adaptive default
+    assert np.array_equal(y, want)
+    for stage, streams in ((8, 1), (8 * 1024 + 8, 2), (1 << 20, 3), (5 << 20, 8)):
+        e.set_pipeline(stage, streams)
+        y[:] = 0
+        e.ecb_host(0, x.ctypes.data, y.ctypes.data, x.nbytes)
+        assert np.array_equal(y, want), (stage, streams)
+    e.close()
