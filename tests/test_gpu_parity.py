@@ -367,7 +367,7 @@ def test_pipeline_shapes_give_identical_bytes(eng, oracle):
     y = np.empty_like(x)
     e.ecb_host(0, x.ctypes.data, y.ctypes.data, x.nbytes)  # adaptive default
     assert np.array_equal(y, want)
-    for stage, streams in ((8, 1), (8 * 1024 + 8, 2), (1 << 20, 3), (5 << 20, 8)):
+    for stage, streams in ((64 << 10, 1), (8 * 1024 * 9 + 8, 2), (1 << 20, 3), (5 << 20, 8)):
         e.set_pipeline(stage, streams)
         y[:] = 0
         e.ecb_host(0, x.ctypes.data, y.ctypes.data, x.nbytes)
