@@ -80,6 +80,12 @@ static int g_gate_sel = 0;     /* internal gates tried as mux selectors at depth
 static int g_pair_tries = 0;   /* pair splits LUT3(a, b, g) tried per node */
 static int g_pair_depth = 0;   /* ... down to this depth */
 static uint64_t g_rng = 88172645463325252ull;
+/* Feistel mode (SBOXGEN_FEISTEL=1): output o is h(outs[2o], outs[2o+1]) for
+ * any 2-input h.  The kernel's Feistel update L' = L ^ y is a lop3 anyway,
+ * so LOP3(L, a, b) = L ^ h(a, b) computes the output's last step for free. */
+static int g_feistel = 0;
+static int g_nout = 4;        /* signals kept alive: 4, or 8 in Feistel mode */
+static int g_top_tries = 8;   /* candidate free-top partners per output */
 
 static uint64_t rnd(void) {
     g_rng ^= g_rng << 13;
@@ -398,7 +404,7 @@ static int fanouts(const circ_t* c, const int* outs, int* fo) {
     memset(fo, 0, sizeof(int) * MAXG);
     for (int g = 6; g < c->n; g++)
         for (int k = 0; k < 3; k++) fo[c->in[g][k]]++;
-    for (int o = 0; o < 4; o++) fo[outs[o]]++;
+    for (int o = 0; o < g_nout; o++) fo[outs[o]]++;
     return 0;
 }
 
@@ -420,7 +426,7 @@ static void sweep(circ_t* c, int* outs) {
         for (int g = 6; g < c->n; g++)
             for (int k = 0; k < 3; k++)
                 if (c->in[g][k] > dead) c->in[g][k]--;
-        for (int o = 0; o < 4; o++)
+        for (int o = 0; o < g_nout; o++)
             if (outs[o] > dead) outs[o]--;
     }
 }
@@ -480,7 +486,7 @@ static int mffc(const circ_t* c, const int* outs, int h, int* in_cone) {
             for (int y = x + 1; y < c->n; y++)
                 if (in_cone[y]) uses_in += (c->in[y][0] == x) + (c->in[y][1] == x) + (c->in[y][2] == x);
             int is_out = 0;
-            for (int o = 0; o < 4; o++) is_out |= outs[o] == x;
+            for (int o = 0; o < g_nout; o++) is_out |= outs[o] == x;
             if (!is_out && uses_in == fo[x]) { in_cone[x] = 1; size++; }
         }
     }
@@ -586,14 +592,14 @@ static int rewrite2(circ_t* c, int* outs) {
             }
         }
         if (order_pass > 2) continue;
-        int nouts[4];
+        int nouts[8];
         int okk = 1;
-        for (int o = 0; o < 4; o++) {
+        for (int o = 0; o < g_nout; o++) {
             nouts[o] = map[outs[o]];
             if (nouts[o] < 0) okk = 0;
         }
         if (!okk) continue;
-        for (int o = 0; o < 4; o++) {
+        for (int o = 0; o < g_nout; o++) {
             tt_t d = r.tt[nouts[o]] ^ c->tt[outs[o]];
             if (d != 0 && d != ~0ull) okk = 0;
         }
@@ -663,8 +669,8 @@ static int rewrite_cone(circ_t* c, int* outs, int tries) {
                 map[g] = add_gate(&r, a, b, cc, l);
             }
             if (bad) continue;
-            int nouts[4];
-            for (int o = 0; o < 4; o++) {
+            int nouts[8];
+            for (int o = 0; o < g_nout; o++) {
                 nouts[o] = map[outs[o]];
                 if (nouts[o] < 0) bad = 1;
                 else {
@@ -692,15 +698,80 @@ static tt_t out_tt(int box, int bit) {
     return t;
 }
 
+/* Do the kept signals realise the four S-box outputs (up to inversion, or
+ * as a 2-input function of the pair in Feistel mode)? */
+static int outputs_ok(const circ_t* c, const int* outs, const tt_t* tgt) {
+    for (int o = 0; o < 4; o++) {
+        if (g_feistel) {
+            uint8_t l;
+            tt_t A = c->tt[outs[2 * o]], B = c->tt[outs[2 * o + 1]];
+            if (!find_lut3(A, B, B, tgt[o], ~0ull, &l)) return 0;
+        } else {
+            tt_t d = c->tt[outs[o]] ^ tgt[o];
+            if (d != 0 && d != ~0ull) return 0;
+        }
+    }
+    return 1;
+}
+
+/* Feistel mode: build output T as h(a, b) with h free.  Tries an existing
+ * pair first, then g_top_tries candidates: plain (a = input 0, b = T) or a
+ * random existing partner a, with b only constrained on the a-cells where T
+ * is not constant (b = T or T ^ a there).  Keeps the smallest. */
+static int build_top(circ_t* st, tt_t T, int* pa, int* pb) {
+    const int n = st->n;
+    for (int a = 0; a < n; a++)
+        for (int b = a + 1; b < n; b++) {
+            uint8_t l;
+            if (find_lut3(st->tt[a], st->tt[b], st->tt[b], T, ~0ull, &l)) { *pa = a; *pb = b; return 0; }
+        }
+    circ_t best;
+    best.n = 1 << 30;
+    int best_a = -1, best_b = -1;
+    for (int t = 0; t < g_top_tries; t++) {
+        int a = t == 0 ? -1 : (int)(rnd() % (unsigned)n);
+        tt_t tgt = T, care = ~0ull;
+        if (a >= 0) {
+            tt_t A = st->tt[a];
+            int m0 = (T & ~A) != 0 && (T & ~A) != ~A;
+            int m1 = (T & A) != 0 && (T & A) != A;
+            care = (m0 ? ~A : 0) | (m1 ? A : 0);
+            if (m0 && m1 && (rnd() & 1)) tgt = T ^ A;
+        }
+        circ_t c = *st;
+        int g = build(&c, tgt, care, 0x3F, 0);
+        if (g < 0) continue;
+        if (c.n < best.n) { best = c; best_a = a < 0 ? 0 : a; best_b = g; }
+    }
+    if (best_b < 0) return -1;
+    *st = best;
+    *pa = best_a;
+    *pb = best_b;
+    return 1;
+}
+
 static void dump(const char* path, int box, const circ_t* c, const int* outs, const tt_t* tgt) {
     FILE* f = path ? fopen(path, "w") : stdout;
     if (!f) return;
     fprintf(f, "box %d gates %d\n", box, c->n - 6);
     for (int g = 6; g < c->n; g++)
         fprintf(f, "g %d %d %d %d 0x%02x\n", g, c->in[g][0], c->in[g][1], c->in[g][2], c->lut[g]);
-    for (int o = 0; o < 4; o++) {
-        tt_t d = c->tt[outs[o]] ^ tgt[o];
-        fprintf(f, "o %d %d %d\n", o, outs[o], d == 0 ? 0 : 1);
+    if (g_feistel) {
+        /* f <out> <a> <b> <h>: output = h(a, b), h bit (2A + B) */
+        for (int o = 0; o < 4; o++) {
+            tt_t A = c->tt[outs[2 * o]], B = c->tt[outs[2 * o + 1]];
+            unsigned h = 0;
+            for (int q = 0; q < 4; q++) {
+                tt_t cell = ((q & 2) ? A : ~A) & ((q & 1) ? B : ~B);
+                if (cell & tgt[o]) h |= 1u << q;
+            }
+            fprintf(f, "f %d %d %d 0x%x\n", o, outs[2 * o], outs[2 * o + 1], h);
+        }
+    } else {
+        for (int o = 0; o < 4; o++) {
+            tt_t d = c->tt[outs[o]] ^ tgt[o];
+            fprintf(f, "o %d %d %d\n", o, outs[o], d == 0 ? 0 : 1);
+        }
     }
     if (path) fclose(f);
 }
@@ -725,7 +796,11 @@ static int load_circuit(const char* path, circ_t* c, int* outs) {
             if (g != c->n) { fclose(f); return 0; }
             add_gate(c, a, b, cc, (uint8_t)lut);
         } else if (sscanf(line, "o %d %d %d", &o, &g, &inv) == 3) {
-            outs[o] = g;
+            if (g_feistel) { outs[2 * o] = 0; outs[2 * o + 1] = g; }
+            else outs[o] = g;
+        } else if (g_feistel && sscanf(line, "f %d %d %d", &o, &a, &b) == 3) {
+            outs[2 * o] = a;
+            outs[2 * o + 1] = b;
         }
     }
     fclose(f);
@@ -734,7 +809,7 @@ static int load_circuit(const char* path, circ_t* c, int* outs) {
 
 static void local_search(int box, long iters, const char* init, const char* out_path, const tt_t* tgt) {
     circ_t best;
-    int best_out[4];
+    int best_out[8];
     if (!load_circuit(init, &best, best_out)) {
         fprintf(stderr, "cannot load %s\n", init);
         exit(2);
@@ -756,7 +831,7 @@ static void local_search(int box, long iters, const char* init, const char* out_
     int record = best.n;
     for (long it = 0; it < iters; it++) {
         circ_t c = best;
-        int outs[4];
+        int outs[8];
         memcpy(outs, best_out, sizeof outs);
         /* rip up 1 or 2 outputs: point them at input 0 so their exclusive
          * gates become dead, sweep, then rebuild them in random order */
@@ -764,7 +839,10 @@ static void local_search(int box, long iters, const char* init, const char* out_
         int which[2];
         which[0] = (int)(rnd() % 4);
         which[1] = (which[0] + 1 + (int)(rnd() % 3)) % 4;
-        for (int j = 0; j < k; j++) outs[which[j]] = 0;
+        for (int j = 0; j < k; j++) {
+            if (g_feistel) outs[2 * which[j]] = outs[2 * which[j] + 1] = 0;
+            else outs[which[j]] = 0;
+        }
         sweep(&c, outs);
         g_budget = best.n + 2;  /* allow near misses; cone resynthesis may shrink them */
         g_deep5 = (rnd() & 1);
@@ -777,6 +855,10 @@ static void local_search(int box, long iters, const char* init, const char* out_
         const int swap = k == 2 && (rnd() & 1);
         for (int j = 0; j < k && ok; j++) {
             int o = which[swap ? 1 - j : j];
+            if (g_feistel) {
+                if (build_top(&c, tgt[o], &outs[2 * o], &outs[2 * o + 1]) < 0) ok = 0;
+                continue;
+            }
             int g = build(&c, tgt[o], ~0ull, 0x3F, 0);
             if (g < 0) ok = 0;
             else outs[o] = g;
@@ -792,11 +874,7 @@ static void local_search(int box, long iters, const char* init, const char* out_
             }
             g_budget = saved;
         }
-        int valid = 1;
-        for (int o = 0; o < 4; o++) {
-            tt_t d = c.tt[outs[o]] ^ tgt[o];
-            if (d != 0 && d != ~0ull) valid = 0;
-        }
+        int valid = outputs_ok(&c, outs, tgt);
         if (!valid) { fprintf(stderr, "internal error: invalid circuit\n"); exit(3); }
         if (c.n <= best.n) {
             best = c;
@@ -819,6 +897,11 @@ int main(int argc, char** argv) {
     long iters = atol(argv[2]);
     g_rng ^= (uint64_t)atoll(argv[3]) * 0x9E3779B97F4A7C15ull;
     if (!g_rng) g_rng = 1;
+    if (getenv("SBOXGEN_FEISTEL") && atoi(getenv("SBOXGEN_FEISTEL"))) {
+        g_feistel = 1;
+        g_nout = 8;
+        if (getenv("SBOXGEN_TOP_TRIES")) g_top_tries = atoi(getenv("SBOXGEN_TOP_TRIES"));
+    }
     int cap = argc > 4 ? atoi(argv[4]) : 60;
     const char* out_path = argc > 5 ? argv[5] : NULL;
     tt_t tgt[4];
@@ -828,7 +911,7 @@ int main(int argc, char** argv) {
         return 0;
     }
     circ_t best;
-    int best_out[4] = {0};
+    int best_out[8] = {0};
     best.n = 1 << 30;
     for (long it = 0; it < iters; it++) {
         circ_t c;
@@ -856,8 +939,12 @@ int main(int argc, char** argv) {
             int j = (int)(rnd() % (unsigned)(i + 1));
             int t = ord[i]; ord[i] = ord[j]; ord[j] = t;
         }
-        int outs[4], ok = 1;
+        int outs[8], ok = 1;
         for (int k = 0; k < 4 && ok; k++) {
+            if (g_feistel) {
+                if (build_top(&c, tgt[ord[k]], &outs[2 * ord[k]], &outs[2 * ord[k] + 1]) < 0) ok = 0;
+                continue;
+            }
             int g = build(&c, tgt[ord[k]], ~0ull, 0x3F, 0);
             if (g < 0) ok = 0;
             outs[ord[k]] = g;
@@ -873,6 +960,7 @@ int main(int argc, char** argv) {
             }
             g_budget = saved;
         }
+        if (!outputs_ok(&c, outs, tgt)) { fprintf(stderr, "internal error: invalid circuit\n"); exit(3); }
         if (c.n < best.n) {
             best = c;
             memcpy(best_out, outs, sizeof outs);
