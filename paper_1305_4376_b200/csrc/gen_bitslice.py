@@ -90,7 +90,32 @@ def load_circuit(box: int, path: str | None = None):
                 gates.append((int(t[1]), int(t[2]), int(t[3]), int(t[4]), int(t[5], 16)))
             elif t[0] == "o":
                 outs[int(t[1])] = (int(t[2]), int(t[3]))
+            elif t[0] == "f":  # output = h(a, b), h bit (2A + B): Feistel top
+                o, a, b, h = int(t[1]), int(t[2]), int(t[3]), int(t[4], 16)
+                if h in (0xA, 0x5):  # h = b or ~b: a plain output
+                    outs[o] = (b, int(h == 0x5))
+                elif h in (0xC, 0x3):  # h = a or ~a
+                    outs[o] = (a, int(h == 0x3))
+                else:
+                    outs[o] = ("f", a, b, h)
     return gates, outs
+
+
+def out_value(val: dict, o) -> int:
+    if o[0] == "f":
+        _, a, b, h = o
+        return (h >> (2 * val[a] + val[b])) & 1
+    g, inv = o
+    return val[g] ^ inv
+
+
+def feistel_lut(h: int) -> int:
+    """LOP3 immediate of L ^ h(a, b) over (L, a, b)."""
+    lut = 0
+    for m in range(8):
+        L, a, b = (m >> 2) & 1, (m >> 1) & 1, m & 1
+        lut |= (L ^ ((h >> (2 * a + b)) & 1)) << m
+    return lut
 
 
 def lut_apply(lut: int, a: int, b: int, c: int) -> int:
@@ -105,8 +130,7 @@ def verify_circuit(box: int, gates, outs) -> None:
             val[g] = lut_apply(lut, val[a], val[b], val[c])
         s = sbox_value(box, six)
         for o in range(4):
-            g, inv = outs[o]
-            if (val[g] ^ inv) != ((s >> o) & 1):
+            if out_value(val, outs[o]) != ((s >> o) & 1):
                 raise SystemExit(f"circuit for S{box + 1} wrong at six={six} bit {o}")
 
 
@@ -144,7 +168,7 @@ def gen_round(circuits) -> list[str]:
     out.append("//   k[32..47] : D, XORed into the 16 duplicated E slots")
     out.append("//   k[48..63] : S = D | 1, for the FMA-pipe form x ^ D = x * S + D")
     out.append("template <int OPT, class KP>")
-    out.append("T3_FI void t3_round(uint32_t (&L)[32], const uint32_t (&R)[32], const KP k) {")
+    out.append("T3_FI void t3_round(uint32_t (&L)[32], const uint32_t (&R)[32], const T3Fk fk, const KP k) {")
     for box in range(8):
         gates, outs = circuits[box]
         out.append(f"  {{  // S{box + 1}: {len(gates)} lop3")
@@ -162,9 +186,15 @@ def gen_round(circuits) -> list[str]:
             out.append(f"    const uint32_t g{g} = lop3<0x{lut:02x}>({names[a]}, {names[b]}, {names[c]});")
             names[g] = f"g{g}"
         for o in range(4):
-            g, inv = outs[o]
             pos = 4 * box + 4 - o  # FIPS position in the 32-bit S output
             p = pos_to_p[pos]
+            if outs[o][0] == "f":
+                # Feistel top: the output's last step h(a, b) merges into the
+                # Feistel lop3; C moves to the FMA pipe (t3_cfix, 2 IMAD).
+                _, a, b, h = outs[o]
+                out.append(f"    L[{p}] = t3_cfix(lop3<0x{feistel_lut(h):02x}>(L[{p}], {names[a]}, {names[b]}), k[{p}], fk);")
+                continue
+            g, inv = outs[o]
             lut = 0x69 if inv else 0x96  # a^b^c (or its complement)
             out.append(f"    L[{p}] = lop3<0x{lut:02x}>(L[{p}], {names[g]}, k[{p}]);")
         out.append("  }")
@@ -199,8 +229,18 @@ def gen_gathers() -> list[str]:
 def main() -> None:
     circuits = []
     total = 0
+    ftops = 0
+    # T3_GEN_FEISTEL_ALL=1 (testing): every output in Feistel-top form
+    # h(a, b) = b, so the FMA-pipe C path runs for all 32 outputs.
+    force = os.environ.get("T3_GEN_FEISTEL_ALL") == "1"
     for box in range(8):
         gates, outs = load_circuit(box)
+        if force:
+            for o in range(4):
+                if outs[o][0] != "f":
+                    g, inv = outs[o]
+                    outs[o] = ("f", 0, g, 0x5 if inv else 0xA)
+        ftops += sum(1 for o in range(4) if outs[o][0] == "f")
         verify_circuit(box, gates, outs)
         circuits.append((gates, outs))
         total += len(gates)
@@ -213,6 +253,8 @@ def main() -> None:
         "// verified exhaustively (64 inputs x 4 outputs) against the FIPS tables.",
         "#pragma once",
         f"#define T3_SBOX_LOP3_TOTAL {total}",
+        f"// outputs whose last gate is merged into the Feistel lop3 (C on the FMA pipe)",
+        f"#define T3_FEISTEL_TOPS {ftops}",
         "",
     ]
     body = hdr + gen_gathers() + [""] + gen_round(circuits) + [""]

@@ -171,6 +171,8 @@ void build_bitslice_table(const std::uint64_t seq[48], T3BsTable& tab, int nroun
     for (int i = 0; i < 32; ++i) tab.w[T3_TAB_WS + 64 + i] = tab.w[T3_TAB_RW1 + i] | 1u;
     for (int i = 0; i < 32; ++i) tab.w[T3_TAB_WS + 96 + i] = tab.w[T3_TAB_RW2 + i] | 1u;
     for (int i = 0; i < 64; ++i) tab.w[T3_TAB_WS + 128 + i] = tab.w[T3_TAB_POST + i] | 1u;
+    tab.w[T3_TAB_FK] = 2u;  // t3_cfix's opaque constants
+    tab.w[T3_TAB_FK + 1] = 1u;
 }
 
 int collapsed_sequence(const std::uint64_t sub48[48], bool decrypt, std::uint64_t seq16[16]) {

@@ -70,6 +70,28 @@ T3_FI uint32_t t3_dfix(uint32_t x, uint32_t d, uint32_t s) {
     return x ^ d;
 }
 
+// x ^ c for a warp-uniform word c in {0, ~0}, entirely on the FMA pipe and
+// with c as the only per-round operand (a uniform register, no LDC):
+//   x ^ c = c * (2x + 1) + x      (c = 0: x;  c = -1: -x - 1 = ~x)
+// Both IMADs take the opaque registers two/one (read from the table) so
+// ptxas cannot strength-reduce 2x + 1 into an ALU LEA.  Used where an
+// S-box output's last gate is merged into the Feistel lop3 (gen_bitslice.py
+// "Feistel tops"), which leaves no lop3 input free for the C word.
+struct T3Fk {
+    uint32_t two, one;
+};
+T3_FI uint32_t t3_cfix(uint32_t x, uint32_t c, T3Fk fk) {
+#ifdef __CUDA_ARCH__
+    uint32_t t, r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(x), "r"(fk.two), "r"(fk.one));
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(t), "r"(c), "r"(x));
+    return r;
+#else
+    (void)fk;
+    return x ^ c;
+#endif
+}
+
 // a >> S; OPT & SHRFMA uses IMAD.HI (a * 2^(32-S) >> 32) on the FMA pipe.
 template <int S, int OPT>
 T3_FI uint32_t t3_shr(uint32_t a) {
@@ -86,7 +108,7 @@ T3_FI uint32_t t3_shr(uint32_t a) {
 #include "generated/bitslice_rounds.cuh"
 
 // ---- whitening/key table (built on the host, schedule.cpp) --------------
-// Word offsets inside the 3456-word table that travels as the kernel's
+// Word offsets inside the 3458-word table that travels as the kernel's
 // __grid_constant__ parameter (constant bank 0, read through LDCU).
 enum : int {
     T3_TAB_PRE = 0,            // 64: initial whitening, half A then half B
@@ -96,7 +118,8 @@ enum : int {
     T3_TAB_RW2 = T3_TAB_RW1 + 32,  // 32: re-whitening of B between pass 2 and 3
     T3_TAB_POST = T3_TAB_RW2 + 32, // 64: final un-whitening, A then B
     T3_TAB_WS = T3_TAB_POST + 64,  // 192: S = D | 1 for PRE(64), RW1(32), RW2(32), POST(64)
-    T3_TAB_WORDS = T3_TAB_WS + 192,
+    T3_TAB_FK = T3_TAB_WS + 192,   // 2: the opaque constants 2, 1 of t3_cfix
+    T3_TAB_WORDS = T3_TAB_FK + 2,
 };
 
 struct T3BsTable {
@@ -167,12 +190,13 @@ template <int OPT, int ROUNDS = 48, class KP>
 T3_FI void t3_cipher(uint32_t (&A)[32], uint32_t (&B)[32], const KP w) {
     // A is written (round 1) before it is ever read, so its initial whitening
     // is 0 by construction (checked in build_bitslice_table); only B needs it.
+    const T3Fk fk{w[T3_TAB_FK], w[T3_TAB_FK + 1]};
     t3_xor_table<OPT>(B, w + T3_TAB_PRE + 32, w + T3_TAB_WS + 32);
     if (ROUNDS == 16) {  // collapsed EDE (single DES): one pass, [A<-B, B<-A] x 8
 #pragma unroll 1
         for (int r = 0; r < 16; r += 2) {
-            t3_round<OPT>(A, B, w + T3_TAB_ROUND + r * T3_ROUND_WORDS);
-            t3_round<OPT>(B, A, w + T3_TAB_ROUND + (r + 1) * T3_ROUND_WORDS);
+            t3_round<OPT>(A, B, fk, w + T3_TAB_ROUND + r * T3_ROUND_WORDS);
+            t3_round<OPT>(B, A, fk, w + T3_TAB_ROUND + (r + 1) * T3_ROUND_WORDS);
         }
         t3_xor_table<OPT>(A, w + T3_TAB_POST, w + T3_TAB_WS + 128);
         return;
@@ -185,8 +209,8 @@ T3_FI void t3_cipher(uint32_t (&A)[32], uint32_t (&B)[32], const KP w) {
 #if T3_BODY_ROUNDS == 4
     // 4-round body: [AB AB]x4, B, [AB AB]x3, [AB], A, [AB AB]x4
     auto body2 = [&](int r) {
-        t3_round<OPT>(A, B, w + T3_TAB_ROUND + r * T3_ROUND_WORDS);
-        t3_round<OPT>(B, A, w + T3_TAB_ROUND + (r + 1) * T3_ROUND_WORDS);
+        t3_round<OPT>(A, B, fk, w + T3_TAB_ROUND + r * T3_ROUND_WORDS);
+        t3_round<OPT>(B, A, fk, w + T3_TAB_ROUND + (r + 1) * T3_ROUND_WORDS);
     };
     int r = 0;
 #pragma unroll 1
@@ -196,11 +220,11 @@ T3_FI void t3_cipher(uint32_t (&A)[32], uint32_t (&B)[32], const KP w) {
         r += 4;
         if (it == 3) {  // after round 15
             t3_xor_table<OPT>(A, w + T3_TAB_RW1, w + T3_TAB_WS + 64);
-            t3_round<OPT>(B, A, w + T3_TAB_ROUND + 16 * T3_ROUND_WORDS);
+            t3_round<OPT>(B, A, fk, w + T3_TAB_ROUND + 16 * T3_ROUND_WORDS);
             r = 17;
         } else if (it == 6) {  // rounds 17..28 done: 29, 30, then 31 = A <- B
             body2(29);
-            t3_round<OPT>(A, B, w + T3_TAB_ROUND + 31 * T3_ROUND_WORDS);
+            t3_round<OPT>(A, B, fk, w + T3_TAB_ROUND + 31 * T3_ROUND_WORDS);
             t3_xor_table<OPT>(B, w + T3_TAB_RW2, w + T3_TAB_WS + 96);
             r = 32;
         }
@@ -209,15 +233,15 @@ T3_FI void t3_cipher(uint32_t (&A)[32], uint32_t (&B)[32], const KP w) {
     int r = 0;
 #pragma unroll 1
     for (int it = 0; it < 23; ++it) {
-        t3_round<OPT>(A, B, w + T3_TAB_ROUND + r * T3_ROUND_WORDS);
-        t3_round<OPT>(B, A, w + T3_TAB_ROUND + (r + 1) * T3_ROUND_WORDS);
+        t3_round<OPT>(A, B, fk, w + T3_TAB_ROUND + r * T3_ROUND_WORDS);
+        t3_round<OPT>(B, A, fk, w + T3_TAB_ROUND + (r + 1) * T3_ROUND_WORDS);
         r += 2;
         if (it == 7) {  // after round 15: pass 2 starts with B <- A
             t3_xor_table<OPT>(A, w + T3_TAB_RW1, w + T3_TAB_WS + 64);
-            t3_round<OPT>(B, A, w + T3_TAB_ROUND + 16 * T3_ROUND_WORDS);
+            t3_round<OPT>(B, A, fk, w + T3_TAB_ROUND + 16 * T3_ROUND_WORDS);
             r = 17;
         } else if (it == 14) {  // after round 30: pass 2 ends with A <- B
-            t3_round<OPT>(A, B, w + T3_TAB_ROUND + 31 * T3_ROUND_WORDS);
+            t3_round<OPT>(A, B, fk, w + T3_TAB_ROUND + 31 * T3_ROUND_WORDS);
             t3_xor_table<OPT>(B, w + T3_TAB_RW2, w + T3_TAB_WS + 96);
             r = 32;
         }

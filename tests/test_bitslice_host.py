@@ -73,10 +73,12 @@ def test_whitening_table_primary_slots(oracle):
     w = (ctypes.c_uint32 * 8192)()
     nw = lib.bs_host_table(s, 0, w)
     # layout (t3des_core.cuh T3_TAB_*): PRE 64 | 48 rounds x 64 | RW1 32 | RW2 32 | POST 64 | S words 192
+    # | t3_cfix constants 2, 1
     stride = 64
     rw1 = 64 + 48 * stride
     rw2, post, ws = rw1 + 32, rw1 + 64, rw1 + 128
-    assert nw == ws + 192
+    assert nw == ws + 192 + 2
+    assert list(w[ws + 192: ws + 194]) == [2, 1]
     w = np.array(w[:nw], dtype=np.uint64)
     for dst, src, n in ((ws, 0, 64), (ws + 64, rw1, 32), (ws + 96, rw2, 32), (ws + 128, post, 64)):
         assert np.array_equal(w[dst:dst + n], w[src:src + n] | 1)  # FMA multipliers S = D | 1

@@ -714,6 +714,24 @@ static int outputs_ok(const circ_t* c, const int* outs, const tt_t* tgt) {
     return 1;
 }
 
+/* Search cost in quarter gates: a real Feistel top (h depends on both a
+ * and b) moves the round's C word to two FMA-pipe IMADs (t3_cfix), measured
+ * at ~0.75 of a lop3 on the saturated ALU pipe (scripts/gpu_ab_feistel.sh). */
+static int g_top_cost = 3;
+static int circuit_cost(const circ_t* c, const int* outs, const tt_t* tgt) {
+    int cost = 4 * (c->n - 6);
+    if (!g_feistel) return cost;
+    for (int o = 0; o < 4; o++) {
+        tt_t A = c->tt[outs[2 * o]], B = c->tt[outs[2 * o + 1]];
+        tt_t d = B ^ tgt[o];
+        if (d == 0 || d == ~0ull) continue;  /* h = b or ~b */
+        d = A ^ tgt[o];
+        if (d == 0 || d == ~0ull) continue;  /* h = a or ~a */
+        cost += g_top_cost;
+    }
+    return cost;
+}
+
 /* Feistel mode: build output T as h(a, b) with h free.  Tries an existing
  * pair first, then g_top_tries candidates: plain (a = input 0, b = T) or a
  * random existing partner a, with b only constrained on the a-cells where T
@@ -828,7 +846,7 @@ static void local_search(int box, long iters, const char* init, const char* out_
     }
     fprintf(stderr, "box %d after rewriting: %d gates\n", box, best.n - 6);
     dump(out_path, box, &best, best_out, tgt);
-    int record = best.n;
+    int record = circuit_cost(&best, best_out, tgt);
     for (long it = 0; it < iters; it++) {
         circ_t c = best;
         int outs[8];
@@ -876,12 +894,13 @@ static void local_search(int box, long iters, const char* init, const char* out_
         }
         int valid = outputs_ok(&c, outs, tgt);
         if (!valid) { fprintf(stderr, "internal error: invalid circuit\n"); exit(3); }
-        if (c.n <= best.n) {
+        const int cost = circuit_cost(&c, outs, tgt);
+        if (cost <= circuit_cost(&best, best_out, tgt)) {
             best = c;
             memcpy(best_out, outs, sizeof outs);
-            if (c.n < record) {
-                record = c.n;
-                fprintf(stderr, "box %d iter %ld: %d gates\n", box, it, c.n - 6);
+            if (cost < record) {
+                record = cost;
+                fprintf(stderr, "box %d iter %ld: %d gates, cost %d\n", box, it, c.n - 6, circuit_cost(&c, outs, tgt));
                 dump(out_path, box, &best, best_out, tgt);
             }
         }
@@ -901,6 +920,7 @@ int main(int argc, char** argv) {
         g_feistel = 1;
         g_nout = 8;
         if (getenv("SBOXGEN_TOP_TRIES")) g_top_tries = atoi(getenv("SBOXGEN_TOP_TRIES"));
+        if (getenv("SBOXGEN_TOP_COST")) g_top_cost = atoi(getenv("SBOXGEN_TOP_COST"));
     }
     int cap = argc > 4 ? atoi(argv[4]) : 60;
     const char* out_path = argc > 5 ? argv[5] : NULL;
@@ -961,10 +981,10 @@ int main(int argc, char** argv) {
             g_budget = saved;
         }
         if (!outputs_ok(&c, outs, tgt)) { fprintf(stderr, "internal error: invalid circuit\n"); exit(3); }
-        if (c.n < best.n) {
+        if (best.n == (1 << 30) || circuit_cost(&c, outs, tgt) < circuit_cost(&best, best_out, tgt)) {
             best = c;
             memcpy(best_out, outs, sizeof outs);
-            fprintf(stderr, "box %d iter %ld: %d gates\n", box, it, c.n - 6);
+            fprintf(stderr, "box %d iter %ld: %d gates, cost %d\n", box, it, c.n - 6, circuit_cost(&c, outs, tgt));
             if (out_path) dump(out_path, box, &best, best_out, tgt);
         }
     }
