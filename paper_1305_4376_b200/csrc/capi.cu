@@ -94,6 +94,21 @@ int launch_bitslice(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8
                         : c->variant == T3DES_CU_VARIANT_BITSLICE_ALU ? 0
                         : c->variant == T3DES_CU_VARIANT_BITSLICE_DFMA ? T3_OPT_DFMA
                                                                        : T3_OPT_SHRFMA;
+#ifdef T3_KEYED_EXPERIMENT
+        if (tma && c->variant == T3DES_CU_VARIANT_BITSLICE) {
+            const int kthreads = T3_KEYED_WARPS * 32;
+            const int smem = T3_KEYED_WARPS * T3_TILE_BLOCKS * 8;
+            static bool attr = false;
+            if (!attr) {
+                T3_CK(cudaFuncSetAttribute(t3_bs_keyed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                attr = true;
+            }
+            std::uint64_t kgrid = 148;
+            if (const char* e = std::getenv("T3_KEYED_GRID")) kgrid = std::strtoull(e, nullptr, 10);
+            t3_bs_keyed_kernel<<<unsigned(kgrid), kthreads, smem, s>>>(in, out, full);
+            return 0;
+        }
+#endif
         if (tma && c->rounds == 16 && opt == T3_OPT_DEFAULT_VALUE) {
             // collapsed EDE (K1 = K2 or K2 = K3): single DES, a third of the work
             t3_bs_tma_kernel<T3_OPT_DEFAULT_VALUE, 16>

@@ -202,6 +202,61 @@ def gen_round(circuits) -> list[str]:
     return out
 
 
+def lut_flip_inputs(lut: int, flips: int) -> int:
+    """LUT of f(a ^ fa, b ^ fb, c ^ fc); flips bit 2/1/0 = a/b/c (minterm index order)."""
+    return sum(((lut >> (m ^ flips)) & 1) << m for m in range(8))
+
+
+def l_role(t: int) -> int:
+    """0 if half A plays L in round t, else 1 (schedule.cpp build_bitslice_table)."""
+    p, loc = divmod(t, 16)
+    a = loc % 2
+    return 1 - a if p == 1 else a
+
+
+def gen_keyed_cipher(circuits, seq, name="t3_cipher_keyed", sync_every=0) -> list[str]:
+    """All len(seq) rounds unrolled with the round keys folded into the lop3
+    immediates: a key bit of 1 on an S-box input complements that input in
+    the LUT of every gate reading it.  No whitening, no key table, no FMA-pipe
+    corrections; Feistel tops merge for free (C no longer exists)."""
+    nrounds = len(seq)
+    pos_to_p = {P[p]: p for p in range(32)}
+    out = [f"T3_FI void {name}(uint32_t (&A)[32], uint32_t (&B)[32]) {{"]
+    for t in range(nrounds):
+        lh = l_role(t) if nrounds == 48 else t % 2
+        L, R = ("A", "B") if lh == 0 else ("B", "A")
+        k = seq[t]
+        out.append(f"  {{  // round {t}: {L} ^= f({R})")
+        for box in range(8):
+            gates, outs = circuits[box]
+            names = {}
+            kinv = {}
+            for kvar in range(6):
+                j = 6 * box + 5 - kvar
+                names[kvar] = f"{R}[{E[j] - 1}]"
+                kinv[kvar] = (k >> (47 - j)) & 1
+            for g, a, b, c, lut in gates:
+                flips = (kinv.get(a, 0) << 2) | (kinv.get(b, 0) << 1) | kinv.get(c, 0)
+                out.append(f"    const uint32_t s{box}g{g} = lop3<0x{lut_flip_inputs(lut, flips):02x}>({names[a]}, {names[b]}, {names[c]});")
+                names[g] = f"s{box}g{g}"
+            for o in range(4):
+                p = pos_to_p[4 * box + 4 - o]
+                if outs[o][0] == "f":
+                    _, a, b, h = outs[o]
+                    fa, fb = kinv.get(a, 0), kinv.get(b, 0)
+                    h2 = sum(((h >> ((((q >> 1) ^ fa) << 1) | ((q & 1) ^ fb))) & 1) << q for q in range(4))
+                    out.append(f"    {L}[{p}] = lop3<0x{feistel_lut(h2):02x}>({L}[{p}], {names[a]}, {names[b]});")
+                else:
+                    g, inv = outs[o]
+                    inv ^= kinv.get(g, 0)  # an output read straight from an input
+                    out.append(f"    {L}[{p}] = lop3<0x{0x3c ^ (0xff if inv else 0):02x}>({L}[{p}], {names[g]}, 0u);")
+        out.append("  }")
+        if sync_every and (t + 1) % sync_every == 0 and t + 1 < nrounds:
+            out.append("  T3_KEYED_SYNC();")
+    out.append("}")
+    return out
+
+
 def gen_gathers() -> list[str]:
     out = []
     # After IP: L_i = input bit IP[i-1], R_i = input bit IP[31+i]

@@ -1,0 +1,31 @@
+#!/bin/bash
+# Experiment: key-specialised (fully unrolled, key folded into lop3
+# immediates) cipher in lockstep CTAs vs the table-driven shipped kernel,
+# bench key, 1 GiB encrypt.  Sweeps the barrier spacing and the grid.
+cd "$GRAFT_REPO_ROOT" || exit 1
+mkdir -p gpurun_out
+python scripts/profile_kernels.py bitslice > gpurun_out/keyed_base.log 2>&1
+check() {
+python - <<'PY'
+import torch, paper_1305_4376_b200 as t3
+e = t3.Engine(0)
+e.set_schedule(t3.triple_schedule(t3.parse_hex_key("133457799BBCDFF10E329232EA6D0D737CA110454A1A6E57")))
+n = (1 << 30) // 8
+src = torch.empty(8 * n, dtype=torch.uint8, device="cuda"); s = torch.cuda.current_stream().cuda_stream
+e.fill_splitmix(src.data_ptr(), 0, n, 1234, s)
+a = torch.empty_like(src); b = torch.empty_like(src)
+e.set_variant(t3.VARIANT_BITSLICE); e.ecb_device(0, src.data_ptr(), a.data_ptr(), 8 * n, s)
+e.set_variant(t3.VARIANT_SPTABLE); e.ecb_device(0, src.data_ptr(), b.data_ptr(), 8 * n, s)
+torch.cuda.synchronize()
+print("keyed == sptable:", bool(torch.equal(a, b)))
+PY
+}
+for SE in ${SYNCS:-4 2 8}; do
+  T3_KEYED_SYNC_EVERY=$SE python scripts/gen_keyed.py
+  make -B -s -C paper_1305_4376_b200/csrc EXTRA_NVFLAGS="-DT3_KEYED_EXPERIMENT $XFLAGS" > gpurun_out/keyed_make_$SE.log 2>&1; echo "make $SE rc=$?"
+  for G in ${GRIDS:-2048 1024 8192}; do
+    echo "sync_every=$SE grid=$G $(T3_KEYED_GRID=$G timeout 60 python scripts/profile_kernels.py bitslice 2>&1 | tail -1)"
+  done
+  T3_KEYED_GRID=2048 timeout 120 check
+done
+cat gpurun_out/keyed_base.log
