@@ -19,6 +19,7 @@
 #include "t3des_cu.h"
 
 #include "ctx.hpp"
+#include "hoststage.hpp"
 
 namespace {
 
@@ -202,6 +203,99 @@ int ensure_staging(t3des_cu_ctx* c, std::size_t bytes, int n) {
     return T3DES_CU_OK;
 }
 
+// Page-locked (cudaMallocHost / cudaHostRegister) host memory?
+bool host_pinned(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+// Pageable spans (hoststage.hpp): stage k goes through pinned slot k % R and
+// stream st[k % R].  Per iteration the in-pool copies stage k into its slot
+// while the out-pool copies stage k - (R - 1) out of its slot (after that
+// stage's D2H event), then stage k's H2D -> kernel -> D2H is enqueued, so up
+// to R - 1 stages are on the GPU while the host threads copy.  A pinned side
+// (in or out) skips its host copy and DMAs straight from/to the span.
+int ecb_host_staged(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8_t* out, std::size_t len,
+                    bool in_pinned, bool out_pinned) {
+    constexpr int R = t3des_cu_ctx::kHostSlots;
+    std::size_t S = c->pipe_explicit ? c->pipe_chunk : c->stage_bytes;  // t3des_cu_set_pipeline
+    if (const char* e = std::getenv("T3DES_HOST_STAGE_MIB")) S = std::size_t(std::max(1, std::atoi(e))) << 20;
+    S = std::min(S, len);
+    if (S > 8 * T3_TILE_BLOCKS) S -= S % (8 * T3_TILE_BLOCKS);
+    if (c->hbuf_bytes < S) {
+        for (int i = 0; i < R; ++i) {
+            if (c->hev_live[i]) T3_CK(cudaEventSynchronize(c->hev[i]));
+            if (c->hbuf[i]) cudaFreeHost(c->hbuf[i]);
+            if (c->hdev[i]) cudaFree(c->hdev[i]);
+            c->hbuf[i] = c->hdev[i] = nullptr;
+        }
+        c->hbuf_bytes = 0;
+        for (int i = 0; i < R; ++i) {
+            T3_CK(cudaMallocHost(&c->hbuf[i], S));
+            T3_CK(cudaMalloc(&c->hdev[i], S));
+            if (!c->hev[i]) T3_CK(cudaEventCreateWithFlags(&c->hev[i], cudaEventDisableTiming));
+            c->hev_live[i] = false;
+        }
+        c->hbuf_bytes = S;
+    }
+    if (!c->pool_in) {
+        int total = c->copy_threads;
+        if (const char* e = std::getenv("T3DES_HOST_COPY_THREADS")) total = std::atoi(e);
+        // measured on the 16-thread B200 hosts (scripts/gpu_pageable.sh): 12
+        // threads with 4 MiB stages are best (26 GB/s end to end vs 7 GB/s
+        // through the driver's own pageable copies)
+        if (total <= 0) total = std::clamp(int(std::thread::hardware_concurrency()) * 3 / 4, 2, 12);
+        c->pool_in = new t3b::CopyPool((total + 1) / 2);
+        c->pool_out = new t3b::CopyPool(std::max(1, total / 2));
+    }
+    const std::size_t nst = (len + S - 1) / S;
+    auto off = [&](std::size_t k) { return k * S; };
+    auto cnt = [&](std::size_t k) { return std::min(S, len - k * S); };
+    // Errors never return with a copy job in flight (the pools would keep
+    // writing into the caller's buffers): every started job is waited for.
+    int rc = T3DES_CU_OK;
+    auto ck = [&](cudaError_t e) {
+        if (e != cudaSuccess && !rc) rc = T3DES_CU_ERR_CUDA;
+        return rc == T3DES_CU_OK;
+    };
+    for (std::size_t k = 0; k < nst + (R - 1) && !rc; ++k) {
+        const bool stage_in = k < nst;
+        const bool stage_out = k >= std::size_t(R - 1) && !out_pinned;
+        const std::size_t j = k - (R - 1);
+        const int slot = int(k % R);
+        bool in_started = false, out_started = false;
+        if (stage_in && !in_pinned && (!c->hev_live[slot] || ck(cudaEventSynchronize(c->hev[slot])))) {
+            c->pool_in->start(c->hbuf[slot], in + off(k), cnt(k));  // the slot's last D2H is done
+            in_started = true;
+        }
+        if (stage_out && ck(cudaEventSynchronize(c->hev[j % R]))) {
+            c->pool_out->start(out + off(j), c->hbuf[j % R], cnt(j));
+            out_started = true;
+        }
+        if (in_started) c->pool_in->wait();
+        if (stage_in && !rc) {
+            cudaStream_t s = c->st[slot];
+            const std::uint8_t* src = in_pinned ? in + off(k) : c->hbuf[slot];
+            std::uint8_t* dst = out_pinned ? out + off(k) : c->hbuf[slot];
+            const std::size_t n = cnt(k);
+            if (cudaMemcpyAsync(c->hdev[slot], src, n, cudaMemcpyHostToDevice, s) != cudaSuccess) rc = T3DES_CU_ERR_CUDA;
+            if (!rc) rc = run_device(c, dir, c->hdev[slot], c->hdev[slot], n / 8, s);
+            if (!rc && cudaMemcpyAsync(dst, c->hdev[slot], n, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+                rc = T3DES_CU_ERR_CUDA;
+            if (!rc && cudaEventRecord(c->hev[slot], s) != cudaSuccess) rc = T3DES_CU_ERR_CUDA;
+            c->hev_live[slot] = !rc;
+        }
+        if (out_started) c->pool_out->wait();
+    }
+    for (int i = 0; i < R; ++i) ck(cudaStreamSynchronize(c->st[i]));
+    if (rc) (void)cudaGetLastError();
+    return rc;
+}
+
 }  // namespace t3b
 
 using t3b::run_device;
@@ -329,6 +423,13 @@ int t3des_cu_destroy(t3des_cu_ctx* c) {
         if (c->ev_join) cudaEventDestroy(c->ev_join);
         for (auto& b : c->buf)
             if (b) cudaFree(b);
+        for (int i = 0; i < t3des_cu_ctx::kHostSlots; ++i) {
+            if (c->hbuf[i]) cudaFreeHost(c->hbuf[i]);
+            if (c->hdev[i]) cudaFree(c->hdev[i]);
+            if (c->hev[i]) cudaEventDestroy(c->hev[i]);
+        }
+        delete c->pool_in;
+        delete c->pool_out;
         if (c->d_sp) cudaFree(c->d_sp);
         if (c->d_acc) cudaFree(c->d_acc);
         (void)cudaGetLastError();
@@ -392,6 +493,8 @@ int t3des_cu_ecb_host(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uin
     if (rc) return rc;
     if (!len) return T3DES_CU_OK;
     DeviceScope scope(c->device);
+    const bool in_pinned = t3b::host_pinned(in), out_pinned = t3b::host_pinned(out);
+    if (!in_pinned || !out_pinned) return t3b::ecb_host_staged(c, dir, in, out, len, in_pinned, out_pinned);
     // Stage size: as set, or adapted to the batch — about 8 stages, between
     // 8 and 32 MiB (scripts/e2e_size_sweep.py: 32-64 MiB batches gain ~10-30%
     // from 8 MiB stages, >= 256 MiB batches prefer 32 MiB), whole tiles.
@@ -462,6 +565,8 @@ int t3des_cu_ecb_multi(const int* devices, int ndev, const std::uint64_t sub48[4
             if (b1 <= b0) return;
             t3des_cu_ctx* c = nullptr;
             int rc = t3des_cu_create(devices[g], &c);
+            // pageable spans: the host's copy threads are shared by the devices
+            if (!rc) c->copy_threads = std::max(2, int(std::thread::hardware_concurrency()) / ndev);
             if (!rc) rc = t3des_cu_set_schedule(c, sub48);
             if (!rc) rc = t3des_cu_ecb_host(c, dir, in + 8 * b0, out + 8 * b0, 8 * (b1 - b0));
             if (c) t3des_cu_destroy(c);

@@ -13,6 +13,10 @@
 #endif
 #include "t3des_cu.h"
 
+namespace t3b {
+class CopyPool;
+}
+
 struct t3des_cu_ctx {
     int device = 0;
     int sms = 0;
@@ -38,6 +42,18 @@ struct t3des_cu_ctx {
     std::size_t pipe_chunk = std::size_t(32) << 20;  // bytes per pipeline stage (upper bound)
     int pipe_streams = 3;
     bool pipe_explicit = false;  // set by t3des_cu_set_pipeline; else stages adapt to the batch
+    // pageable-span staging (t3des_cu_ecb_host): pinned ring, one event per
+    // slot (the slot's last GPU use), and two host copy pools (in / out)
+    static constexpr int kHostSlots = 4;
+    std::uint8_t* hbuf[kHostSlots] = {};
+    std::uint8_t* hdev[kHostSlots] = {};
+    std::size_t hbuf_bytes = 0;
+    cudaEvent_t hev[kHostSlots] = {};
+    bool hev_live[kHostSlots] = {};
+    t3b::CopyPool* pool_in = nullptr;
+    t3b::CopyPool* pool_out = nullptr;
+    std::size_t stage_bytes = std::size_t(4) << 20;  // pageable stage size
+    int copy_threads = 0;                            // total host copy threads (0 = auto)
     std::uint64_t launches = 0;
     cudaStream_t tail_st = nullptr;             // side stream for the partial tile (AUTO)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -52,5 +68,13 @@ int run_device(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8_t* o
 
 // Make sure the first n staging buffers hold at least `bytes` each.
 int ensure_staging(t3des_cu_ctx* c, std::size_t bytes, int n);
+
+// Page-locked host memory (DMA-able without bouncing)?
+bool host_pinned(const void* p);
+
+// t3des_cu_ecb_host for spans that are not both pinned: pinned ring staging
+// with host copy threads (hoststage.hpp).
+int ecb_host_staged(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8_t* out, std::size_t len,
+                    bool in_pinned, bool out_pinned);
 
 }  // namespace t3b

@@ -357,19 +357,56 @@ def test_auto_variant_with_large_work_group(eng, oracle):
 
 def test_pipeline_shapes_give_identical_bytes(eng, oracle):
     """t3des_cu_set_pipeline: any stage size / stream count (and the adaptive
-    default) produces the same bytes through the host path."""
+    default) produces the same bytes through the host path, from pinned
+    buffers (direct DMA pipeline) and from pageable ones (staged)."""
     ts = t3.triple_schedule(t3.parse_hex_key(BENCH_KEY))
     s = oracle.schedule_hex(BENCH_KEY)
     x = oracle.splitmix(0, (24 << 20) // 8 + 3, 5)
     want = oracle.ecb(x, s, 0)
+    px = torch.from_numpy(x).pin_memory()
+    py = torch.empty(x.nbytes, dtype=torch.uint8).pin_memory()
+    y = np.empty_like(x)
     e = t3.Engine(0)
     e.set_schedule(ts)
-    y = np.empty_like(x)
-    e.ecb_host(0, x.ctypes.data, y.ctypes.data, x.nbytes)  # adaptive default
+    e.ecb_host(0, px.data_ptr(), py.data_ptr(), x.nbytes)  # adaptive default
+    assert np.array_equal(py.numpy(), want)
+    e.ecb_host(0, x.ctypes.data, y.ctypes.data, x.nbytes)
     assert np.array_equal(y, want)
     for stage, streams in ((64 << 10, 1), (8 * 1024 * 9 + 8, 2), (1 << 20, 3), (5 << 20, 8)):
         e.set_pipeline(stage, streams)
+        py.zero_()
+        e.ecb_host(0, px.data_ptr(), py.data_ptr(), x.nbytes)
+        assert np.array_equal(py.numpy(), want), (stage, streams)
         y[:] = 0
         e.ecb_host(0, x.ctypes.data, y.ctypes.data, x.nbytes)
-        assert np.array_equal(y, want), (stage, streams)
+        assert np.array_equal(y, want), ("pageable", stage, streams)
+    e.close()
+
+
+@pytest.mark.parametrize("nblocks", [1, 31, 1025, (8 << 20) // 8 - 1, (8 << 20) // 8 + 1, (40 << 20) // 8 + 77])
+def test_pageable_staging_mixed_and_in_place(oracle, nblocks):
+    """Pageable spans go through the pinned staging ring with host copy
+    threads: pageable/pinned in every combination, in place, sizes around
+    the 8 MiB stage, byte-identical to the oracle."""
+    ts = t3.triple_schedule(t3.parse_hex_key(KEYS[1]))
+    s = oracle.schedule_hex(KEYS[1])
+    x = oracle.splitmix(0, nblocks, 17)
+    want = oracle.ecb(x, s, 0)
+    e = t3.Engine(0)
+    e.set_schedule(ts)
+    pin_in = torch.from_numpy(x).pin_memory()
+    pin_out = torch.empty(x.nbytes, dtype=torch.uint8).pin_memory()
+    page_out = np.zeros_like(x)
+    e.ecb_host(0, x.ctypes.data, page_out.ctypes.data, x.nbytes)  # pageable -> pageable
+    assert np.array_equal(page_out, want)
+    e.ecb_host(0, x.ctypes.data, pin_out.data_ptr(), x.nbytes)  # pageable -> pinned
+    assert np.array_equal(pin_out.numpy(), want)
+    page_out[:] = 0
+    e.ecb_host(0, pin_in.data_ptr(), page_out.ctypes.data, x.nbytes)  # pinned -> pageable
+    assert np.array_equal(page_out, want)
+    z = x.copy()
+    e.ecb_host(0, z.ctypes.data, z.ctypes.data, z.nbytes)  # pageable, in place
+    assert np.array_equal(z, want)
+    e.ecb_host(1, z.ctypes.data, z.ctypes.data, z.nbytes)
+    assert np.array_equal(z, x)
     e.close()
