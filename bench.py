@@ -522,7 +522,8 @@ def main() -> None:
         "bound": "alu", "achieved": round(achieved, 4), "peak": round(peak_tlops, 4), "unit": "Tlop3/s",
         "frac": round(achieved / peak_tlops, 4), "traffic": traffic,
         "kernel_ms": round(ms_step, 4),
-        "peak_source": f"{sms} SMs x {ALU_LANES_PER_CLK_PER_SM} ALU lanes/clk x sm_max_mhz {fmax:.0f} "
+        "peak_source": f"{sms} SMs x {ALU_LANES_PER_CLK_PER_SM} ALU lanes/clk (LOP3 issue rate measured by "
+                       f"tools/microbench/pipe_rates.cu, profiles/r1/pipe_rates_b200.txt) x sm_max_mhz {fmax:.0f} "
                        f"({'MEASURED_PEAKS.json' if 'sm_max_mhz' in peaks else 'fallback'})",
         "frac_at_run_clock": (round(achieved / (sms * 64 * clocks["sm_mhz"] * 1e6 / 1e12), 4)
                               if clocks.get("sm_mhz") else None),
