@@ -114,7 +114,10 @@ int t3des_cu_ecb_device(t3des_cu_ctx* ctx, int direction, const void* din, void*
  * several streams (t3des_cu_set_pipeline); returns when `out` holds the result.  This is the entry
  * a Backend::Cuda branch of run_batch calls (same contract as
  * encrypt_batch/decrypt_batch).  Pinned buffers (t3des_cu_host_alloc)
- * give full PCIe overlap; pageable buffers work, more slowly. */
+ * give full PCIe overlap; pageable spans are staged through a pinned ring
+ * by host copy threads (T3DES_HOST_COPY_THREADS, default 3/4 of the host's
+ * threads, at most 12).  Device memory is rejected (T3DES_CU_ERR_ARG): use
+ * t3des_cu_ecb_device. */
 int t3des_cu_ecb_host(t3des_cu_ctx* ctx, int direction, const uint8_t* in, uint8_t* out,
                       size_t len);
 

@@ -213,6 +213,16 @@ bool host_pinned(const void* p) {
     return a.type == cudaMemoryTypeHost;
 }
 
+// Device memory (not host-accessible): not a valid host span.
+bool device_only(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice;
+}
+
 // Pageable spans (hoststage.hpp): stage k goes through pinned slot k % R and
 // stream st[k % R].  Per iteration the in-pool copies stage k into its slot
 // while the out-pool copies stage k - (R - 1) out of its slot (after that
@@ -493,6 +503,7 @@ int t3des_cu_ecb_host(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uin
     if (rc) return rc;
     if (!len) return T3DES_CU_OK;
     DeviceScope scope(c->device);
+    if (t3b::device_only(in) || t3b::device_only(out)) return T3DES_CU_ERR_ARG;  // use t3des_cu_ecb_device
     const bool in_pinned = t3b::host_pinned(in), out_pinned = t3b::host_pinned(out);
     if (!in_pinned || !out_pinned) return t3b::ecb_host_staged(c, dir, in, out, len, in_pinned, out_pinned);
     // Stage size: as set, or adapted to the batch — about 8 stages, between

@@ -72,6 +72,9 @@ int ensure_staging(t3des_cu_ctx* c, std::size_t bytes, int n);
 // Page-locked host memory (DMA-able without bouncing)?
 bool host_pinned(const void* p);
 
+// Device-only memory (an error for the host entry points)?
+bool device_only(const void* p);
+
 // t3des_cu_ecb_host for spans that are not both pinned: pinned ring staging
 // with host copy threads (hoststage.hpp).
 int ecb_host_staged(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8_t* out, std::size_t len,

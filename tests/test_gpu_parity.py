@@ -409,4 +409,9 @@ def test_pageable_staging_mixed_and_in_place(oracle, nblocks):
     assert np.array_equal(z, want)
     e.ecb_host(1, z.ctypes.data, z.ctypes.data, z.nbytes)
     assert np.array_equal(z, x)
+    d = torch.empty(x.nbytes, dtype=torch.uint8, device="cuda")
+    with pytest.raises(ValueError):  # device memory is not a host span
+        e.ecb_host(0, x.ctypes.data, d.data_ptr(), x.nbytes)
+    with pytest.raises(ValueError):
+        e.ecb_host(0, d.data_ptr(), page_out.ctypes.data, x.nbytes)
     e.close()
