@@ -109,6 +109,8 @@ int t3des_cu_set_launch(t3des_cu_ctx* ctx, size_t chunk_blocks, int work_group);
  * overlap is rejected, len == 0 is a no-op (dispatch.cpp:91-104,215). */
 int t3des_cu_ecb_device(t3des_cu_ctx* ctx, int direction, const void* din, void* dout,
                         size_t len, void* stream);
+/* (Spans that are not 8-byte aligned are bounced through an aligned device
+ * buffer, and the call then returns only when the work is done.) */
 
 /* Host buffers, end to end: chunked H2D -> kernel -> D2H pipelined over
  * several streams (t3des_cu_set_pipeline); returns when `out` holds the result.  This is the entry

@@ -433,6 +433,7 @@ int t3des_cu_destroy(t3des_cu_ctx* c) {
         if (c->ev_join) cudaEventDestroy(c->ev_join);
         for (auto& b : c->buf)
             if (b) cudaFree(b);
+        if (c->ubuf) cudaFree(c->ubuf);
         for (int i = 0; i < t3des_cu_ctx::kHostSlots; ++i) {
             if (c->hbuf[i]) cudaFreeHost(c->hbuf[i]);
             if (c->hdev[i]) cudaFree(c->hdev[i]);
@@ -493,8 +494,24 @@ int t3des_cu_ecb_device(t3des_cu_ctx* c, int dir, const void* din, void* dout, s
     if (rc) return rc;
     if (!len) return T3DES_CU_OK;
     DeviceScope scope(c->device);
-    return run_device(c, dir, static_cast<const std::uint8_t*>(din), static_cast<std::uint8_t*>(dout),
-                      len / 8, static_cast<cudaStream_t>(stream));
+    const auto* in = static_cast<const std::uint8_t*>(din);
+    auto* out = static_cast<std::uint8_t*>(dout);
+    auto s = static_cast<cudaStream_t>(stream);
+    if (((reinterpret_cast<std::uintptr_t>(in) | reinterpret_cast<std::uintptr_t>(out)) & 7u) == 0)
+        return run_device(c, dir, in, out, len / 8, s);
+    // Spans that are not 8-byte aligned (the kernels load whole blocks):
+    // bounce through an aligned device buffer, chunk by chunk, on the
+    // caller's stream; synchronous, so the buffer is free on return.
+    constexpr std::size_t kChunk = std::size_t(16) << 20;
+    if (!c->ubuf) T3_CK(cudaMalloc(&c->ubuf, kChunk));
+    for (std::size_t off = 0; off < len; off += kChunk) {
+        const std::size_t n = std::min(kChunk, len - off);
+        T3_CK(cudaMemcpyAsync(c->ubuf, in + off, n, cudaMemcpyDeviceToDevice, s));
+        if (int rc2 = run_device(c, dir, c->ubuf, c->ubuf, n / 8, s)) return rc2;
+        T3_CK(cudaMemcpyAsync(out + off, c->ubuf, n, cudaMemcpyDeviceToDevice, s));
+    }
+    T3_CK(cudaStreamSynchronize(s));
+    return T3DES_CU_OK;
 }
 
 int t3des_cu_ecb_host(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8_t* out,

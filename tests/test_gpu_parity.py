@@ -300,6 +300,31 @@ def test_64gib_sharding_invariance_on_one_device(eng, oracle):
     assert len(set(sums.values())) == 1, sums
 
 
+@pytest.mark.parametrize("variant", [N.VARIANT_AUTO, N.VARIANT_BITSLICE, N.VARIANT_SPTABLE])
+def test_unaligned_device_spans(eng, oracle, variant):
+    """Device spans at any byte offset (the kernels load whole blocks; such
+    spans are bounced through an aligned buffer), in place and across the
+    16 MiB bounce chunk."""
+    ts = t3.triple_schedule(t3.parse_hex_key(KEYS[0]))
+    s = oracle.schedule_hex(KEYS[0])
+    eng.set_schedule(ts)
+    eng.set_variant(variant)
+    eng.set_launch(0, 0)
+    st = torch.cuda.current_stream().cuda_stream
+    for n, off_in, off_out in ((1, 1, 3), (1025, 3, 4), (8195, 4, 4), ((16 << 20) // 8 + 5, 5, 2)):
+        x = oracle.splitmix(0, n, n)
+        want = oracle.ecb(x, s, 0)
+        a = torch.zeros(8 * n + 16, dtype=torch.uint8, device="cuda")
+        b = torch.zeros(8 * n + 16, dtype=torch.uint8, device="cuda")
+        a[off_in: off_in + 8 * n].copy_(torch.from_numpy(x))
+        eng.ecb_device(0, a.data_ptr() + off_in, b.data_ptr() + off_out, 8 * n, st)
+        torch.cuda.synchronize()
+        assert np.array_equal(b[off_out: off_out + 8 * n].cpu().numpy(), want), (n, off_in, off_out)
+        eng.ecb_device(1, b.data_ptr() + off_out, b.data_ptr() + off_out, 8 * n, st)  # in place
+        torch.cuda.synchronize()
+        assert np.array_equal(b[off_out: off_out + 8 * n].cpu().numpy(), x), (n, "in place")
+
+
 @pytest.mark.parametrize("variant", VARIANTS)
 def test_no_writes_outside_the_batch(eng, oracle, variant):
     """Sentinel bytes before and after the output range survive every
