@@ -631,7 +631,8 @@ int t3des_cu_ecb_multi_device(const int* devices, int ndev, const std::uint64_t 
         DeviceScope scope(devices[g]);
         cudaStream_t s = ctx[g]->st[0];
         const std::size_t bytes = 8 * count;
-        if (devices[g] == home && !(flags & T3DES_CU_MULTI_STAGE_ALL)) {
+        const bool aligned = ((reinterpret_cast<std::uintptr_t>(in) | reinterpret_cast<std::uintptr_t>(out)) & 7u) == 0;
+        if (devices[g] == home && !(flags & T3DES_CU_MULTI_STAGE_ALL) && aligned) {
             rc = run_device(ctx[g], dir, in + 8 * first, out + 8 * first, count, s);
             continue;
         }

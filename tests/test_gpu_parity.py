@@ -368,6 +368,12 @@ def test_multi_device_resident_scatter_gather(oracle):
     # in place, decrypt
     rc = N.lib().t3des_cu_ecb_multi_device(arr, len(devs), s, 1, 0, dst.data_ptr(), dst.data_ptr(), x.nbytes, 1)
     assert rc == 0 and np.array_equal(host(dst), x)
+    # spans that are not 8-byte aligned: the home shard is staged too
+    a = torch.zeros(x.nbytes + 8, dtype=torch.uint8, device="cuda")
+    a[3: 3 + x.nbytes].copy_(src)
+    b = torch.zeros_like(a)
+    rc = N.lib().t3des_cu_ecb_multi_device(arr, len(devs), s, 0, 0, a.data_ptr() + 3, b.data_ptr() + 5, x.nbytes, 0)
+    assert rc == 0 and np.array_equal(b[5: 5 + x.nbytes].cpu().numpy(), oracle.ecb(x, s, 0))
 
 
 def test_auto_variant_with_large_work_group(eng, oracle):
