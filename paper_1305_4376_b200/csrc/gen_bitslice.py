@@ -156,6 +156,11 @@ def e_slot_maps():
     return prim_slot, secondary
 
 
+# E-duplicate corrections that may go to the FMA pipe (bit d = D word d);
+# the default is all 16 (measured best).
+DFMA_MASK = int(os.environ.get("T3_GEN_DFMA_MASK", "0xFFFF"), 0)
+
+
 def gen_round(circuits) -> list[str]:
     prim_slot, secondary = e_slot_maps()
     d_index = {j: i for i, j in enumerate(secondary)}
@@ -178,7 +183,10 @@ def gen_round(circuits) -> list[str]:
             q = E[j] - 1
             if j in d_index:
                 nm = f"x{kvar}"
-                out.append(f"    const uint32_t {nm} = t3_dfix<OPT>(R[{q}], k[{32 + d_index[j]}], k[{48 + d_index[j]}]);")
+                if (DFMA_MASK >> d_index[j]) & 1:
+                    out.append(f"    const uint32_t {nm} = t3_dfix<OPT>(R[{q}], k[{32 + d_index[j]}], k[{48 + d_index[j]}]);")
+                else:  # kept on the ALU pipe (T3_GEN_DFMA_MASK experiments)
+                    out.append(f"    const uint32_t {nm} = R[{q}] ^ k[{32 + d_index[j]}];")
                 names[kvar] = nm
             else:
                 names[kvar] = f"R[{q}]"
