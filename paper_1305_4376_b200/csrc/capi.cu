@@ -23,7 +23,7 @@
 
 namespace {
 
-constexpr int kSpSmemBytes = 8 * 64 * 32 * 4;                   // 64 KiB
+constexpr int kSpSmemBytes = 8 * 64 * 32 * 4 + 48 * 8 * 4 + 8 * 64 * 4;  // 64 KiB tables, round keys, staging
 
 // Restores the caller's current device on scope exit.
 struct DeviceScope {
@@ -155,7 +155,7 @@ int launch_sptable(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8_
     const bool single = c->rounds == 16;
     t3_sp_kernel<<<unsigned(std::max<std::uint64_t>(grid, 1)), threads, kSpSmemBytes, s>>>(
         reinterpret_cast<const uint2*>(in), reinterpret_cast<uint2*>(out), nblocks, c->d_sp, single ? 1 : 3,
-        single ? c->sp16[dir] : c->sp[dir]);
+        c->d_spk + (single ? 2 + dir : dir) * 48 * 8);
     T3_CK(cudaGetLastError());
     ++c->launches;
     return T3DES_CU_OK;
@@ -434,6 +434,7 @@ int t3des_cu_destroy(t3des_cu_ctx* c) {
         for (auto& b : c->buf)
             if (b) cudaFree(b);
         if (c->ubuf) cudaFree(c->ubuf);
+        if (c->d_spk) cudaFree(c->d_spk);
         for (int i = 0; i < t3des_cu_ctx::kHostSlots; ++i) {
             if (c->hbuf[i]) cudaFreeHost(c->hbuf[i]);
             if (c->hdev[i]) cudaFree(c->hdev[i]);
@@ -467,6 +468,18 @@ int t3des_cu_set_schedule(t3des_cu_ctx* c, const std::uint64_t sub48[48]) {
             t3b::build_sp_keys(seq16, k);
             std::memcpy(c->sp16[dir].k, k.k, sizeof k.k);
         }
+    }
+    // device copy of the SP-table kernel's round keys (sp[enc], sp[dec],
+    // sp16[enc], sp16[dec]); it stages them in shared memory
+    {
+        DeviceScope scope(c->device);
+        if (!c->d_spk) {
+            T3_CK(cudaMalloc(&c->d_spk, 4 * sizeof(T3SpKeyParam)));
+        } else {
+            T3_CK(cudaDeviceSynchronize());  // no launch may still read the old keys
+        }
+        const T3SpKeyParam keys[4] = {c->sp[0], c->sp[1], c->sp16[0], c->sp16[1]};
+        T3_CK(cudaMemcpy(c->d_spk, keys, sizeof keys, cudaMemcpyHostToDevice));
     }
     c->have_schedule = true;
     return T3DES_CU_OK;

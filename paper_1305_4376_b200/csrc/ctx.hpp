@@ -54,6 +54,7 @@ struct t3des_cu_ctx {
     t3b::CopyPool* pool_out = nullptr;
     std::size_t stage_bytes = std::size_t(4) << 20;  // pageable stage size
     int copy_threads = 0;                            // total host copy threads (0 = auto)
+    std::uint32_t* d_spk = nullptr;  // device copies of sp[2], sp16[2] (48 x 8 words each)
     std::uint8_t* ubuf = nullptr;  // bounce buffer for device spans that are not 8-byte aligned
     std::uint64_t launches = 0;
     cudaStream_t tail_st = nullptr;             // side stream for the partial tile (AUTO)

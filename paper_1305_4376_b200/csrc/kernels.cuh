@@ -233,11 +233,23 @@ __device__ __forceinline__ uint32_t t3_sp_f(uint32_t r, const uint32_t* k, const
     return f;
 }
 
+// The 48 x 8 round-key words are staged in shared memory next to the tables
+// (from a device copy): read from the constant bank, every round's keys miss
+// the constant cache once per CTA, which dominates small launches.
 __global__ void __launch_bounds__(T3_SP_THREADS)
 t3_sp_kernel(const uint2* in, uint2* out, uint64_t nblocks, const uint32_t* __restrict__ sp_global,
-             int passes, const __grid_constant__ T3SpKeyParam kp) {
+             int passes, const uint32_t* __restrict__ keys_global) {
     extern __shared__ uint32_t t3_sp_smem[];
-    for (int w = threadIdx.x; w < 8 * 64 * 32; w += blockDim.x) t3_sp_smem[w] = sp_global[w >> 5];
+    uint32_t* ks = t3_sp_smem + 8 * 64 * 32;  // [48][8]
+    uint32_t* sp = ks + 48 * 8;               // the 2 KiB table, staged once
+    // one global round trip: every thread issues its few loads together, then
+    // the 32-fold lane replication is a shared-memory copy (a fill loop of 64
+    // dependent-latency global loads per thread cost ~7 us per launch)
+    for (int w = threadIdx.x; w < 48 * 8; w += blockDim.x) ks[w] = __ldg(keys_global + w);
+    for (int w = threadIdx.x; w < 8 * 64; w += blockDim.x) sp[w] = __ldg(sp_global + w);
+    __syncthreads();
+#pragma unroll 8
+    for (int w = threadIdx.x; w < 8 * 64 * 32; w += blockDim.x) t3_sp_smem[w] = sp[w >> 5];
     __syncthreads();
     const char* smem_lane = reinterpret_cast<const char*>(t3_sp_smem) + (threadIdx.x & 31) * 4;
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
@@ -253,19 +265,19 @@ t3_sp_kernel(const uint2* in, uint2* out, uint64_t nblocks, const uint32_t* __re
         t3_dswap(x, y, 1, 0x55555555u);
 #pragma unroll 1
         for (int t = 0; t < 16; t += 2) {
-            x ^= t3_sp_f(y, kp.k[t], smem_lane);
-            y ^= t3_sp_f(x, kp.k[t + 1], smem_lane);
+            x ^= t3_sp_f(y, ks + 8 * t, smem_lane);
+            y ^= t3_sp_f(x, ks + 8 * (t + 1), smem_lane);
         }
         if (passes == 3) {  // 1 = collapsed EDE (single DES)
 #pragma unroll 1
             for (int t = 16; t < 32; t += 2) {
-                y ^= t3_sp_f(x, kp.k[t], smem_lane);
-                x ^= t3_sp_f(y, kp.k[t + 1], smem_lane);
+                y ^= t3_sp_f(x, ks + 8 * t, smem_lane);
+                x ^= t3_sp_f(y, ks + 8 * (t + 1), smem_lane);
             }
 #pragma unroll 1
             for (int t = 32; t < 48; t += 2) {
-                x ^= t3_sp_f(y, kp.k[t], smem_lane);
-                y ^= t3_sp_f(x, kp.k[t + 1], smem_lane);
+                x ^= t3_sp_f(y, ks + 8 * t, smem_lane);
+                y ^= t3_sp_f(x, ks + 8 * (t + 1), smem_lane);
             }
         }
         // preoutput = y || x, then FP = the IP swaps in reverse order.
