@@ -23,7 +23,8 @@
 
 namespace {
 
-constexpr int kSpSmemBytes = 8 * 64 * 32 * 4 + 48 * 8 * 4 + 8 * 64 * 4;  // 64 KiB tables, round keys, staging
+constexpr std::uint64_t kSpBigCtaMinBlocks = 16384;  // 128 KiB
+constexpr int kSpSmemBytes = 8 * 64 * 32 * 4 + int(sizeof(T3SpKeyParam)) + 8 * 64 * 4;  // 64 KiB tables, round keys, staging
 
 // Restores the caller's current device on scope exit.
 struct DeviceScope {
@@ -147,15 +148,60 @@ int launch_bitslice(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8
     return T3DES_CU_OK;
 }
 
+// SP-table kernel instances (T3_SPV_* code-generation masks) compiled in.
+#define T3_SPV_LIST(X) X(0) X(T3_SPV_DEFAULT)
+
+const void* sp_kernel_fn(int spv) {
+    switch (spv) {
+#define T3_SPV_FN(V) \
+    case V: return reinterpret_cast<const void*>(&t3_sp_kernel<V>);
+        T3_SPV_LIST(T3_SPV_FN)
+#undef T3_SPV_FN
+        default: return nullptr;
+    }
+}
+
+T3SpMul sp_mul() {
+    T3SpMul m{};
+    m.one = 1;
+    for (int i = 1; i <= 4; ++i) m.m[i] = 1u << (32 - (20 - 4 * i));
+    m.m[6] = 16;
+    return m;
+}
+
 int launch_sptable(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8_t* out,
                    std::uint64_t nblocks, cudaStream_t s) {
-    const int threads = c->work_group > 0 ? c->work_group : T3_SP_THREADS;
+    // CTA size: 1024 threads (2 CTAs = 64 warps per SM, and the 64 KiB table
+    // fill split 4x finer) unless the batch is too small to give every SM a
+    // CTA, where 256-thread CTAs spread it wider (scripts/sp_variant_sweep.py:
+    // 1 GiB 160 vs 140 GB/s; 8 KiB 8.2 vs 12.4 us)
+    const int threads = c->work_group > 0                     ? c->work_group
+                        : nblocks >= kSpBigCtaMinBlocks       ? T3_SP_THREADS_BIG
+                                                              : T3_SP_THREADS;
     std::uint64_t grid = (nblocks + threads - 1) / threads;
-    grid = std::min<std::uint64_t>(grid, std::uint64_t(c->sms) * std::uint64_t(c->sp_occ));
+    int occ = threads == T3_SP_THREADS ? c->sp_occ : threads == T3_SP_THREADS_BIG ? c->sp_occ_big : 0;
+    if (!occ &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sp_kernel_fn(c->sp_var), threads, kSpSmemBytes) != cudaSuccess)
+        return T3DES_CU_ERR_CUDA;
+    grid = std::min<std::uint64_t>(grid, std::uint64_t(c->sms) * std::uint64_t(std::max(occ, 1)));
     const bool single = c->rounds == 16;
-    t3_sp_kernel<<<unsigned(std::max<std::uint64_t>(grid, 1)), threads, kSpSmemBytes, s>>>(
-        reinterpret_cast<const uint2*>(in), reinterpret_cast<uint2*>(out), nblocks, c->d_sp, single ? 1 : 3,
-        c->d_spk + (single ? 2 + dir : dir) * 48 * 8);
+    const auto* sin = reinterpret_cast<const uint2*>(in);
+    auto* sout = reinterpret_cast<uint2*>(out);
+    const int passes = single ? 1 : 3;
+    const std::uint32_t* keys = c->d_spk + (single ? 2 + dir : dir) * (sizeof(T3SpKeyParam) / 4);
+    const T3SpKeyParam& kp = single ? c->sp16[dir] : c->sp[dir];
+    static const T3SpMul mul = sp_mul();
+    const unsigned g = unsigned(std::max<std::uint64_t>(grid, 1));
+    switch (c->sp_var) {
+#define T3_SPV_CASE(V)                                                                                \
+    case V:                                                                                           \
+        t3_sp_kernel<V><<<g, threads, kSpSmemBytes, s>>>(sin, sout, nblocks, c->d_sp, passes, keys, mul, kp); \
+        break;
+        T3_SPV_LIST(T3_SPV_CASE)
+#undef T3_SPV_CASE
+        default:
+            return T3DES_CU_ERR_ARG;
+    }
     T3_CK(cudaGetLastError());
     ++c->launches;
     return T3DES_CU_OK;
@@ -381,9 +427,22 @@ int t3des_cu_create(int device, t3des_cu_ctx** out) {
             rc = T3DES_CU_ERR_CUDA;
             break;
         }
-        if (cudaFuncSetAttribute(t3_sp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kSpSmemBytes) != cudaSuccess ||
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->sp_occ, t3_sp_kernel, T3_SP_THREADS,
+        // Tuning override (experiments only): SP-table code-generation mask.
+        if (const char* e = std::getenv("T3DES_SP_VAR")) c->sp_var = std::atoi(e);
+        if (!sp_kernel_fn(c->sp_var)) {
+            rc = T3DES_CU_ERR_ARG;
+            break;
+        }
+        bool attr_ok = true;
+#define T3_SPV_ATTR(V)                                                                               \
+    attr_ok = attr_ok && cudaFuncSetAttribute(t3_sp_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                              kSpSmemBytes) == cudaSuccess;
+        T3_SPV_LIST(T3_SPV_ATTR)
+#undef T3_SPV_ATTR
+        if (!attr_ok ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->sp_occ, sp_kernel_fn(c->sp_var), T3_SP_THREADS,
+                                                          kSpSmemBytes) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->sp_occ_big, sp_kernel_fn(c->sp_var), T3_SP_THREADS_BIG,
                                                           kSpSmemBytes) != cudaSuccess) {
             rc = T3DES_CU_ERR_CUDA;
             break;
@@ -398,6 +457,7 @@ int t3des_cu_create(int device, t3des_cu_ctx** out) {
             if (v > 0) c->bs_ctas_per_sm = v;
         }
         c->sp_occ = std::max(c->sp_occ, 1);
+        c->sp_occ_big = std::max(c->sp_occ_big, 1);
         std::uint32_t sp[8][64];
         t3b::build_sp_tables(sp);
         if (cudaMalloc(&c->d_sp, sizeof sp) != cudaSuccess ||
@@ -460,6 +520,7 @@ int t3des_cu_set_schedule(t3des_cu_ctx* c, const std::uint64_t sub48[48]) {
         t3b::SpKeys k;
         t3b::build_sp_keys(seq, k);
         std::memcpy(c->sp[dir].k, k.k, sizeof k.k);
+        std::memcpy(c->sp[dir].k2, k.k2, sizeof k.k2);
         // K1 = K2 or K2 = K3: the EDE collapses to single DES (16 rounds)
         std::uint64_t seq16[48] = {};
         if (t3b::collapsed_sequence(sub48, dir == T3DES_CU_DECRYPT, seq16) == 16) {
@@ -467,6 +528,7 @@ int t3des_cu_set_schedule(t3des_cu_ctx* c, const std::uint64_t sub48[48]) {
             t3b::build_bitslice_table(seq16, c->bs16[dir], 16);
             t3b::build_sp_keys(seq16, k);
             std::memcpy(c->sp16[dir].k, k.k, sizeof k.k);
+            std::memcpy(c->sp16[dir].k2, k.k2, sizeof k.k2);
         }
     }
     // device copy of the SP-table kernel's round keys (sp[enc], sp[dec],

@@ -23,7 +23,9 @@ struct t3des_cu_ctx {
     int bs_occ = 1;           // resident CTAs per SM (occupancy) of the bitsliced kernel
     int bs_ctas_per_sm = 64;  // grid size of the bitsliced kernel, in CTAs per SM
     int bs_opt = T3_OPT_DEFAULT_VALUE;  // T3_OPT_* mask of the default bitsliced variant
-    int sp_occ = 1;
+    int sp_occ = 1;      // resident SP-table CTAs per SM at T3_SP_THREADS
+    int sp_occ_big = 1;  // ... at T3_SP_THREADS_BIG
+    int sp_var = T3_SPV_DEFAULT;  // T3_SPV_* mask of the SP-table kernel
     bool have_schedule = false;
     int variant = T3DES_CU_VARIANT_AUTO;
     std::size_t chunk_blocks = 0;

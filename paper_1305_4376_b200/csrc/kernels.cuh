@@ -29,7 +29,8 @@
 #ifndef T3_BS_MIN_CTAS
 #define T3_BS_MIN_CTAS 4  // resident CTAs per SM the register budget is sized for
 #endif
-#define T3_SP_THREADS 256
+#define T3_SP_THREADS 256        // SP-table CTA size for small batches
+#define T3_SP_THREADS_BIG 1024  // ... and for batches of >= 16384 blocks
 #define T3_TILE_BLOCKS 1024  // blocks per warp tile (32 lanes x 32 blocks)
 #ifndef T3_OPT_DEFAULT
 #define T3_OPT_DEFAULT T3_OPT_DFMA  // for the LDG/tail kernels; the TMA kernel's mask is per context
@@ -219,39 +220,137 @@ __device__ __forceinline__ void t3_dswap(uint32_t& a, uint32_t& b, int s, uint32
     a ^= w << s;
 }
 
+// Code-generation options of the SP-table kernel (template bitmask SPV).
+// Per round the kernel extracts 8 six-bit windows of R (rotate), XORs the
+// round-key chunk and masks (one lop3), adds the lane's table column, loads,
+// and merges the 8 table words into L.  Everything but the loads runs on the
+// ALU pipe unless these options move work to the (otherwise idle) FMA pipe.
+// Measured (scripts/sp_variant_sweep.py, profiles/r1/sp_variants_r1k.txt).
+enum : int {
+    T3_SPV_LANEFMA = 1,  // lane column added as IMAD (else a lop3 OR)
+    T3_SPV_MERGE6 = 2,   // the 8 table words summed by 6 IMADs (disjoint bits: + = |), 1 lop3 into L
+    T3_SPV_MERGE4 = 4,   // 4 IMADs + 2 lop3 (else 4 lop3)
+    T3_SPV_SHLFMA = 8,   // S-box 6's window (a left shift by 4) as IMAD, else a funnel rotate
+    T3_SPV_SHRFMA = 16,  // S-boxes 1-4 windows (right shifts) as IMAD.HI, else funnel rotates
+    T3_SPV_KEYPARAM = 32, // 48 rounds unrolled, round keys as uniform constant-bank operands (LDCU)
+    T3_SPV_KEY2 = 64,     // key XOR on R (2 words, t3b::SpKeys::k2) instead of on the 8 windows;
+                          // the lane column then merges into the mask lop3
+};
+
+// Opaque multipliers of the FMA-pipe forms (kernel parameter: ptxas cannot
+// strength-reduce a multiply by an unknown value back into an ALU shift/OR).
+struct T3SpMul {
+    uint32_t one;   // 1
+    uint32_t m[8];  // S-box i: 2^(32-s) for the right shift s = 20-4i (i = 1..4), 16 for i = 6
+};
+
+__device__ __forceinline__ uint32_t t3_mad(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+__device__ __forceinline__ uint32_t t3_mulhi(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+
 // Shared-memory table layout: word (i * 64 + six) * 32 + lane, i.e. byte
 // offset i*8192 + six*128 + lane*4.  Keys arrive pre-shifted to bits 7..12.
-__device__ __forceinline__ uint32_t t3_sp_f(uint32_t r, const uint32_t* k, const char* smem_lane) {
-    uint32_t f = 0;
+// Returns L ^ f(R, k) (f = the fused S/P round function).
+template <int SPV>
+__device__ __forceinline__ uint32_t t3_sp_round(uint32_t l, uint32_t r, const uint32_t* ks, const char* smem,
+                                                uint32_t lane4, const T3SpMul& mul) {
+    // the round's 8 key words: two broadcast LDS.128 (shared) or uniform
+    // constant-bank operands (kernel parameter, compile-time round index)
+    if (SPV & T3_SPV_KEY2) {  // ks -> {Ka, Kb}
+        const uint32_t ra = r ^ ks[0], rb = r ^ ks[1];
+        uint32_t v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint32_t ri = (i & 1) ? rb : ra;
+            uint32_t y;
+            if ((SPV & T3_SPV_SHLFMA) && i == 6)
+                y = t3_mad(ri, mul.m[6], 0u);  // ri << 4
+            else
+                y = __funnelshift_r(ri, ri, (20 - 4 * i) & 31);
+            const uint32_t col = (y & 0x1F80u) | lane4;  // one lop3
+            v[i] = *reinterpret_cast<const uint32_t*>(smem + i * 8192 + col);
+        }
+        if (SPV & T3_SPV_MERGE6) {
+            const uint32_t a = t3_mad(t3_mad(v[0], mul.one, v[1]), mul.one, t3_mad(v[2], mul.one, v[3]));
+            const uint32_t b = t3_mad(t3_mad(v[4], mul.one, v[5]), mul.one, t3_mad(v[6], mul.one, v[7]));
+            return l ^ a ^ b;
+        }
+        if (SPV & T3_SPV_MERGE4) {
+            const uint32_t a = t3_mad(v[0], mul.one, v[1]), b = t3_mad(v[2], mul.one, v[3]);
+            const uint32_t c = t3_mad(v[4], mul.one, v[5]), d = t3_mad(v[6], mul.one, v[7]);
+            return l ^ (a | b | c) ^ d;
+        }
+        return l ^ ((v[0] | v[1] | v[2]) | (v[3] | v[4] | v[5]) | (v[6] | v[7]));
+    }
+    uint32_t k[8];
+    if (SPV & T3_SPV_KEYPARAM) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) k[i] = ks[i];
+    } else {
+        const uint4 ka = reinterpret_cast<const uint4*>(ks)[0], kb = reinterpret_cast<const uint4*>(ks)[1];
+        k[0] = ka.x, k[1] = ka.y, k[2] = ka.z, k[3] = ka.w, k[4] = kb.x, k[5] = kb.y, k[6] = kb.z, k[7] = kb.w;
+    }
+    uint32_t v[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        // E window of S-box i rotated so its 6 bits sit at bits 7..12.
-        const uint32_t y = __funnelshift_r(r, r, (20 - 4 * i) & 31);
+        // E window of S-box i moved so its 6 bits sit at bits 7..12.
+        uint32_t y;
+        if ((SPV & T3_SPV_SHRFMA) && i >= 1 && i <= 4)
+            y = t3_mulhi(r, mul.m[i]);  // r >> (20 - 4i)
+        else if ((SPV & T3_SPV_SHLFMA) && i == 6)
+            y = t3_mad(r, mul.m[6], 0u);  // r << 4
+        else
+            y = __funnelshift_r(r, r, (20 - 4 * i) & 31);
         const uint32_t off = (y ^ k[i]) & 0x1F80u;
-        f |= *reinterpret_cast<const uint32_t*>(smem_lane + i * 8192 + off);
+        const uint32_t col = (SPV & T3_SPV_LANEFMA) ? t3_mad(off, mul.one, lane4) : (off | lane4);
+        v[i] = *reinterpret_cast<const uint32_t*>(smem + i * 8192 + col);
     }
-    return f;
+    // the 8 words have disjoint bits (each S-box owns 4 output bits): sums are ORs
+    if (SPV & T3_SPV_MERGE6) {
+        const uint32_t a = t3_mad(t3_mad(v[0], mul.one, v[1]), mul.one, t3_mad(v[2], mul.one, v[3]));
+        const uint32_t b = t3_mad(t3_mad(v[4], mul.one, v[5]), mul.one, t3_mad(v[6], mul.one, v[7]));
+        return l ^ a ^ b;
+    }
+    if (SPV & T3_SPV_MERGE4) {
+        const uint32_t a = t3_mad(v[0], mul.one, v[1]), b = t3_mad(v[2], mul.one, v[3]);
+        const uint32_t c = t3_mad(v[4], mul.one, v[5]), d = t3_mad(v[6], mul.one, v[7]);
+        return l ^ (a | b | c) ^ d;
+    }
+    return l ^ ((v[0] | v[1] | v[2]) | (v[3] | v[4] | v[5]) | (v[6] | v[7]));
 }
 
 // The 48 x 8 round-key words are staged in shared memory next to the tables
 // (from a device copy): read from the constant bank, every round's keys miss
 // the constant cache once per CTA, which dominates small launches.
-__global__ void __launch_bounds__(T3_SP_THREADS)
+#define T3_SPK(kp, t) ((SPV & T3_SPV_KEY2) ? (kp).k2[t] : (kp).k[t])
+#define T3_SKS(t) ((SPV & T3_SPV_KEY2) ? ks2 + 2 * (t) : ks + 8 * (t))
+template <int SPV>
+__global__ void __launch_bounds__(1024)
 t3_sp_kernel(const uint2* in, uint2* out, uint64_t nblocks, const uint32_t* __restrict__ sp_global,
-             int passes, const uint32_t* __restrict__ keys_global) {
-    extern __shared__ uint32_t t3_sp_smem[];
+             int passes, const uint32_t* __restrict__ keys_global, const __grid_constant__ T3SpMul mul,
+             const __grid_constant__ T3SpKeyParam kp) {
+    extern __shared__ __align__(16) uint32_t t3_sp_smem[];
     uint32_t* ks = t3_sp_smem + 8 * 64 * 32;  // [48][8]
-    uint32_t* sp = ks + 48 * 8;               // the 2 KiB table, staged once
+    uint32_t* sp = ks + sizeof(T3SpKeyParam) / 4;  // the 2 KiB table, staged once
     // one global round trip: every thread issues its few loads together, then
     // the 32-fold lane replication is a shared-memory copy (a fill loop of 64
     // dependent-latency global loads per thread cost ~7 us per launch)
-    for (int w = threadIdx.x; w < 48 * 8; w += blockDim.x) ks[w] = __ldg(keys_global + w);
+    for (int w = threadIdx.x; w < int(sizeof(T3SpKeyParam) / 4); w += blockDim.x) ks[w] = __ldg(keys_global + w);
+    const uint32_t* ks2 = ks + 48 * 8;  // T3SpKeyParam::k2
     for (int w = threadIdx.x; w < 8 * 64; w += blockDim.x) sp[w] = __ldg(sp_global + w);
     __syncthreads();
 #pragma unroll 8
     for (int w = threadIdx.x; w < 8 * 64 * 32; w += blockDim.x) t3_sp_smem[w] = sp[w >> 5];
     __syncthreads();
-    const char* smem_lane = reinterpret_cast<const char*>(t3_sp_smem) + (threadIdx.x & 31) * 4;
+    const char* smem = reinterpret_cast<const char*>(t3_sp_smem);
+    const uint32_t lane4 = (threadIdx.x & 31) * 4;
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
     for (uint64_t b = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < nblocks; b += stride) {
         const uint2 v = __ldcs(in + b);
@@ -263,22 +362,42 @@ t3_sp_kernel(const uint2* in, uint2* out, uint64_t nblocks, const uint32_t* __re
         t3_dswap(y, x, 2, 0x33333333u);
         t3_dswap(y, x, 8, 0x00FF00FFu);
         t3_dswap(x, y, 1, 0x55555555u);
+        if (SPV & T3_SPV_KEYPARAM) {
+#pragma unroll
+            for (int t = 0; t < 16; t += 2) {
+                x = t3_sp_round<SPV>(x, y, T3_SPK(kp, t), smem, lane4, mul);
+                y = t3_sp_round<SPV>(y, x, T3_SPK(kp, t + 1), smem, lane4, mul);
+            }
+            if (passes == 3) {
+#pragma unroll
+                for (int t = 16; t < 32; t += 2) {
+                    y = t3_sp_round<SPV>(y, x, T3_SPK(kp, t), smem, lane4, mul);
+                    x = t3_sp_round<SPV>(x, y, T3_SPK(kp, t + 1), smem, lane4, mul);
+                }
+#pragma unroll
+                for (int t = 32; t < 48; t += 2) {
+                    x = t3_sp_round<SPV>(x, y, T3_SPK(kp, t), smem, lane4, mul);
+                    y = t3_sp_round<SPV>(y, x, T3_SPK(kp, t + 1), smem, lane4, mul);
+                }
+            }
+        } else {
 #pragma unroll 1
         for (int t = 0; t < 16; t += 2) {
-            x ^= t3_sp_f(y, ks + 8 * t, smem_lane);
-            y ^= t3_sp_f(x, ks + 8 * (t + 1), smem_lane);
+            x = t3_sp_round<SPV>(x, y, T3_SKS(t), smem, lane4, mul);
+            y = t3_sp_round<SPV>(y, x, T3_SKS(t + 1), smem, lane4, mul);
         }
         if (passes == 3) {  // 1 = collapsed EDE (single DES)
 #pragma unroll 1
-            for (int t = 16; t < 32; t += 2) {
-                y ^= t3_sp_f(x, ks + 8 * t, smem_lane);
-                x ^= t3_sp_f(y, ks + 8 * (t + 1), smem_lane);
+            for (int t = 16; t < 32; t += 2) {  // pass 2: roles swapped
+                y = t3_sp_round<SPV>(y, x, T3_SKS(t), smem, lane4, mul);
+                x = t3_sp_round<SPV>(x, y, T3_SKS(t + 1), smem, lane4, mul);
             }
 #pragma unroll 1
             for (int t = 32; t < 48; t += 2) {
-                x ^= t3_sp_f(y, ks + 8 * t, smem_lane);
-                y ^= t3_sp_f(x, ks + 8 * (t + 1), smem_lane);
+                x = t3_sp_round<SPV>(x, y, T3_SKS(t), smem, lane4, mul);
+                y = t3_sp_round<SPV>(y, x, T3_SKS(t + 1), smem, lane4, mul);
             }
+        }
         }
         // preoutput = y || x, then FP = the IP swaps in reverse order.
         uint32_t hi = y, lo = x;

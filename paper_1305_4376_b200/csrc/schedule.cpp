@@ -188,9 +188,16 @@ int collapsed_sequence(const std::uint64_t sub48[48], bool decrypt, std::uint64_
 }
 
 void build_sp_keys(const std::uint64_t seq[48], SpKeys& out) {
-    for (int t = 0; t < 48; ++t)
-        for (int i = 0; i < 8; ++i)
-            out.k[t][i] = static_cast<std::uint32_t>((seq[t] >> (42 - 6 * i)) & 0x3F) << 7;
+    for (int t = 0; t < 48; ++t) {
+        out.k2[t][0] = out.k2[t][1] = 0;
+        for (int i = 0; i < 8; ++i) {
+            const std::uint32_t kc = static_cast<std::uint32_t>((seq[t] >> (42 - 6 * i)) & 0x3F) << 7;
+            out.k[t][i] = kc;
+            // the kernel reads window i as rotr(R, s) bits 7..12, s = (20 - 4i) mod 32
+            const int s = (20 - 4 * i) & 31;
+            out.k2[t][i & 1] |= s ? (kc << s) | (kc >> (32 - s)) : kc;
+        }
+    }
 }
 
 void build_sp_tables(std::uint32_t sp[8][64]) {

@@ -43,8 +43,12 @@ int collapsed_sequence(const std::uint64_t sub48[48], bool decrypt, std::uint64_
 // Per-round 6-bit key chunks for the SP-table kernel: k6[r][i] is the key
 // input of S-box i in round r, shifted to bits 7..12 (pre-scaled as a byte
 // offset of a 128-byte row).
+// k2[r] = {Ka, Kb}: the same chunks placed at the R-word bit positions their
+// S-box windows read (windows 0,2,4,6 are disjoint, as are 1,3,5,7), so one
+// XOR of R with Ka (Kb) keys four windows at once.
 struct SpKeys {
     std::uint32_t k[48][8];
+    std::uint32_t k2[48][2];
 };
 void build_sp_keys(const std::uint64_t seq[48], SpKeys& out);
 

@@ -130,7 +130,12 @@ struct T3BsTable {
 // t3b::build_sp_keys).
 struct T3SpKeyParam {
     uint32_t k[48][8];
+    uint32_t k2[48][2];  // t3b::SpKeys::k2
 };
+
+#ifndef T3_SPV_DEFAULT
+#define T3_SPV_DEFAULT 106  // T3_SPV_* mask of the SP-table kernel (kernels.cuh): KEY2|KEYPARAM|SHLFMA|MERGE6
+#endif
 
 // In-register transpose of a 32x32 bit matrix: afterwards x[k] bit m is the
 // old x[m] bit k.  Stages 16 and 8 are byte moves (PRMT); stages 4, 2, 1
