@@ -105,6 +105,29 @@ def test_chunk_and_work_group_invariance(eng, oracle):
             assert np.array_equal(run(eng, ts, x, 0, N.VARIANT_SPTABLE, chunk=chunk, wg=wg), want)
 
 
+@pytest.mark.parametrize("spv", [0, 106])
+def test_sptable_codegen_masks_and_cta_sizes(oracle, spv, monkeypatch):
+    """SP-table kernel: the previous round structure (mask 0) and the shipped
+    one (106: key XOR on R, uniform keys, FMA merges), 256- and 1024-thread
+    CTAs (the size rule switches at 16384 blocks) and explicit work groups up
+    to 1024, all keying options, both directions, against the oracle."""
+    monkeypatch.setenv("T3DES_SP_VAR", str(spv))  # read at context creation
+    e = t3.Engine(0)
+    try:
+        for keyhex in KEYS:
+            ts = t3.triple_schedule(t3.parse_hex_key(keyhex))
+            s = oracle.schedule_hex(keyhex)
+            for n in (5, 16383, 16384, 70001):
+                x = np.random.default_rng(n + spv).integers(0, 256, 8 * n, dtype=np.uint8)
+                for d in (0, 1):
+                    want = oracle.ecb(x, s, d)
+                    for wg in (0, 64, 512, 1024):
+                        got = run(e, ts, x, d, N.VARIANT_SPTABLE, wg=wg)
+                        assert np.array_equal(got, want), (keyhex, n, d, wg)
+    finally:
+        e.close()
+
+
 def test_device_errors(eng):
     ts = t3.triple_schedule(t3.parse_hex_key(KEYS[0]))
     eng.set_schedule(ts)
