@@ -340,7 +340,10 @@ int run_bench(const Opts& o) {
         if (o.sweep == "workers") r.workers = static_cast<unsigned>(v);
         if (o.sweep == "chunk") r.chunk = v;
         if (o.sweep == "workgroup") r.wg = v;
-        if (r.wg == 0) r.wg = o.variant == "sptable" ? 256 : 128;  // the kernels' own CTA sizes
+        if (r.wg == 0) {  // the kernels' own CTA sizes (capi.cu launch_sptable / launch_bitslice)
+            const std::uint64_t launch_blocks = r.chunk ? std::min<std::uint64_t>(r.chunk, bytes / 8) : bytes / 8;
+            r.wg = o.variant == "sptable" ? (launch_blocks >= 16384 ? 1024 : 256) : 128;
+        }
         try {
             double best = 0;
             if (o.mode == "device" && r.workers == 1) {
