@@ -216,6 +216,37 @@ int check_batch(t3des_cu_ctx* c, int dir, const void* in, const void* out, std::
     return T3DES_CU_OK;
 }
 
+// Contexts of the multi-GPU entries (t3des_cu_ecb_multi*), kept across
+// calls: creating one costs device queries, table uploads, streams, and its
+// staging buffers are allocated on first use, all of which a per-call
+// context paid again every call.  A context is handed to one caller at a
+// time (calls into a context are serialised).
+std::mutex g_pool_mu;
+std::vector<t3des_cu_ctx*> g_pool;  // idle contexts, any device
+
+int pool_acquire(int device, t3des_cu_ctx** out) {
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        for (auto it = g_pool.begin(); it != g_pool.end(); ++it)
+            if ((*it)->device == device) {
+                *out = *it;
+                g_pool.erase(it);
+                return T3DES_CU_OK;
+            }
+    }
+    return t3des_cu_create(device, out);
+}
+
+void pool_release(t3des_cu_ctx* c, bool healthy) {
+    if (!c) return;
+    if (!healthy) {  // after a CUDA error: do not hand the context out again
+        t3des_cu_destroy(c);
+        return;
+    }
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    g_pool.push_back(c);
+}
+
 }  // namespace
 
 namespace t3b {
@@ -667,12 +698,12 @@ int t3des_cu_ecb_multi(const int* devices, int ndev, const std::uint64_t sub48[4
             const std::uint64_t b1 = b0 + cnt;
             if (b1 <= b0) return;
             t3des_cu_ctx* c = nullptr;
-            int rc = t3des_cu_create(devices[g], &c);
+            int rc = pool_acquire(devices[g], &c);
             // pageable spans: the host's copy threads are shared by the devices
-            if (!rc) c->copy_threads = std::max(2, int(std::thread::hardware_concurrency()) / ndev);
+            if (!rc && !c->pool_in) c->copy_threads = std::max(2, int(std::thread::hardware_concurrency()) / ndev);
             if (!rc) rc = t3des_cu_set_schedule(c, sub48);
             if (!rc) rc = t3des_cu_ecb_host(c, dir, in + 8 * b0, out + 8 * b0, 8 * (b1 - b0));
-            if (c) t3des_cu_destroy(c);
+            pool_release(c, rc == T3DES_CU_OK || rc == T3DES_CU_ERR_ARG);
             rcs[g] = rc;
         });
     }
@@ -700,7 +731,7 @@ int t3des_cu_ecb_multi_device(const int* devices, int ndev, const std::uint64_t 
         std::uint64_t first = 0, count = 0;
         t3des_cu_shard_range(nblocks, ndev, g, &first, &count);
         if (!count) continue;
-        rc = t3des_cu_create(devices[g], &ctx[g]);
+        rc = pool_acquire(devices[g], &ctx[g]);
         if (!rc) rc = t3des_cu_set_schedule(ctx[g], sub48);
         if (rc) break;
         DeviceScope scope(devices[g]);
@@ -731,7 +762,7 @@ int t3des_cu_ecb_multi_device(const int* devices, int ndev, const std::uint64_t 
         DeviceScope scope(devices[g]);
         if (cudaStreamSynchronize(ctx[g]->st[0]) != cudaSuccess && !rc) rc = T3DES_CU_ERR_CUDA;
         if (stage[g]) cudaFree(stage[g]);
-        t3des_cu_destroy(ctx[g]);
+        pool_release(ctx[g], rc == T3DES_CU_OK || rc == T3DES_CU_ERR_ARG);
     }
     (void)cudaGetLastError();
     return rc;
