@@ -188,7 +188,7 @@ int launch_sptable(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8_
     const auto* sin = reinterpret_cast<const uint2*>(in);
     auto* sout = reinterpret_cast<uint2*>(out);
     const int passes = single ? 1 : 3;
-    const std::uint32_t* keys = c->d_spk + (single ? 2 + dir : dir) * (sizeof(T3SpKeyParam) / 4);
+    const std::uint32_t* keys = c->d_spk ? c->d_spk + (single ? 2 + dir : dir) * (sizeof(T3SpKeyParam) / 4) : nullptr;
     const T3SpKeyParam& kp = single ? c->sp16[dir] : c->sp[dir];
     static const T3SpMul mul = sp_mul();
     const unsigned g = unsigned(std::max<std::uint64_t>(grid, 1));
@@ -543,6 +543,10 @@ int t3des_cu_destroy(t3des_cu_ctx* c) {
 
 int t3des_cu_set_schedule(t3des_cu_ctx* c, const std::uint64_t sub48[48]) {
     if (!c || !sub48) return T3DES_CU_ERR_ARG;
+    // the same schedule again (the C++/Python batch APIs install it on every
+    // call): nothing to rebuild, and no device synchronisation
+    if (c->have_schedule && std::memcmp(c->sub48, sub48, sizeof c->sub48) == 0) return T3DES_CU_OK;
+    c->have_schedule = false;  // until every table below is rebuilt
     c->rounds = 48;
     for (int dir = 0; dir < 2; ++dir) {
         std::uint64_t seq[48];
@@ -563,8 +567,10 @@ int t3des_cu_set_schedule(t3des_cu_ctx* c, const std::uint64_t sub48[48]) {
         }
     }
     // device copy of the SP-table kernel's round keys (sp[enc], sp[dec],
-    // sp16[enc], sp16[dec]); it stages them in shared memory
-    {
+    // sp16[enc], sp16[dec]) for the masks that stage them in shared memory;
+    // the shipped mask takes them as a kernel parameter (by value, like the
+    // bitsliced tables), so a new schedule never waits for launches in flight
+    if (!(c->sp_var & T3_SPV_KEYPARAM)) {
         DeviceScope scope(c->device);
         if (!c->d_spk) {
             T3_CK(cudaMalloc(&c->d_spk, 4 * sizeof(T3SpKeyParam)));
@@ -574,6 +580,7 @@ int t3des_cu_set_schedule(t3des_cu_ctx* c, const std::uint64_t sub48[48]) {
         const T3SpKeyParam keys[4] = {c->sp[0], c->sp[1], c->sp16[0], c->sp16[1]};
         T3_CK(cudaMemcpy(c->d_spk, keys, sizeof keys, cudaMemcpyHostToDevice));
     }
+    std::memcpy(c->sub48, sub48, sizeof c->sub48);
     c->have_schedule = true;
     return T3DES_CU_OK;
 }

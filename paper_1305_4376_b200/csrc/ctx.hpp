@@ -27,6 +27,7 @@ struct t3des_cu_ctx {
     int sp_occ_big = 1;  // ... at T3_SP_THREADS_BIG
     int sp_var = T3_SPV_DEFAULT;  // T3_SPV_* mask of the SP-table kernel
     bool have_schedule = false;
+    std::uint64_t sub48[48] = {};  // the installed schedule (pass-major)
     int variant = T3DES_CU_VARIANT_AUTO;
     std::size_t chunk_blocks = 0;
     int work_group = 0;

@@ -342,7 +342,8 @@ t3_sp_kernel(const uint2* in, uint2* out, uint64_t nblocks, const uint32_t* __re
     // one global round trip: every thread issues its few loads together, then
     // the 32-fold lane replication is a shared-memory copy (a fill loop of 64
     // dependent-latency global loads per thread cost ~7 us per launch)
-    for (int w = threadIdx.x; w < int(sizeof(T3SpKeyParam) / 4); w += blockDim.x) ks[w] = __ldg(keys_global + w);
+    if (!(SPV & T3_SPV_KEYPARAM))
+        for (int w = threadIdx.x; w < int(sizeof(T3SpKeyParam) / 4); w += blockDim.x) ks[w] = __ldg(keys_global + w);
     const uint32_t* ks2 = ks + 48 * 8;  // T3SpKeyParam::k2
     for (int w = threadIdx.x; w < 8 * 64; w += blockDim.x) sp[w] = __ldg(sp_global + w);
     __syncthreads();
