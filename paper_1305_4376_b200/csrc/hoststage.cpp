@@ -63,6 +63,12 @@ CopyPool::~CopyPool() {
 }
 
 void CopyPool::start(void* dst, const void* src, std::size_t bytes) {
+    if (bytes <= kInlineBytes) {  // waking the pool costs more than the copy
+        std::memcpy(dst, src, bytes);
+        std::lock_guard<std::mutex> l(m_);
+        left_ = 0;
+        return;
+    }
     {
         std::lock_guard<std::mutex> l(m_);
         dst_ = static_cast<char*>(dst);

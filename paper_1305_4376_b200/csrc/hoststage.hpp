@@ -25,6 +25,8 @@ public:
     ~CopyPool();
     CopyPool(const CopyPool&) = delete;
     CopyPool& operator=(const CopyPool&) = delete;
+    // copies of at most kInlineBytes run on the calling thread
+    static constexpr std::size_t kInlineBytes = std::size_t(64) << 10;
     void start(void* dst, const void* src, std::size_t bytes);
     void wait();
     int threads() const { return n_; }
