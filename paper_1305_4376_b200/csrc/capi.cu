@@ -247,6 +247,19 @@ void pool_release(t3des_cu_ctx* c, bool healthy) {
     g_pool.push_back(c);
 }
 
+// Pipeline stage size for host batches below 64 MiB (pinned and pageable
+// alike): enough stages that copies in, kernels and copies out overlap, but
+// not so many that per-stage costs dominate (scripts/e2e_small_sweep.py,
+// profiles/r1/e2e_small_r1l.txt: 1 MiB best in 2 stages, 4 MiB in 4, 16 MiB
+// in 8-16).  0 = not a small batch (the large-batch rules apply).
+std::size_t small_batch_stage(std::size_t len) {
+    constexpr std::size_t KiB = 1024, MiB = KiB * KiB;
+    if (len >= 64 * MiB) return 0;
+    std::size_t s = len <= 512 * KiB ? len : len <= 2 * MiB ? len / 2 : len <= 8 * MiB ? len / 4 : len / 8;
+    if (s > 8 * T3_TILE_BLOCKS) s -= s % (8 * T3_TILE_BLOCKS);
+    return std::max<std::size_t>(s, 8);
+}
+
 }  // namespace
 
 namespace t3b {
@@ -310,6 +323,7 @@ int ecb_host_staged(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8
                     bool in_pinned, bool out_pinned) {
     constexpr int R = t3des_cu_ctx::kHostSlots;
     std::size_t S = c->pipe_explicit ? c->pipe_chunk : c->stage_bytes;  // t3des_cu_set_pipeline
+    if (!c->pipe_explicit && small_batch_stage(len)) S = small_batch_stage(len);
     if (const char* e = std::getenv("T3DES_HOST_STAGE_MIB")) S = std::size_t(std::max(1, std::atoi(e))) << 20;
     S = std::min(S, len);
     if (S > 8 * T3_TILE_BLOCKS) S -= S % (8 * T3_TILE_BLOCKS);
@@ -643,6 +657,7 @@ int t3des_cu_ecb_host(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uin
     if (!c->pipe_explicit) {
         chunk = std::min(chunk, std::max(std::size_t(8) << 20, len / 8));
         chunk -= chunk % (8 * T3_TILE_BLOCKS);
+        if (const std::size_t s = small_batch_stage(len)) chunk = s;
     }
     chunk = std::min(len, chunk);
     const int ns = c->pipe_streams;
