@@ -235,6 +235,8 @@ enum : int {
     T3_SPV_KEYPARAM = 32, // 48 rounds unrolled, round keys as uniform constant-bank operands (LDCU)
     T3_SPV_KEY2 = 64,     // key XOR on R (2 words, t3b::SpKeys::k2) instead of on the 8 windows;
                           // the lane column then merges into the mask lop3
+    T3_SPV_PREFETCH = 128, // a thread's first block loaded before the table fill, each next
+                           // block before the current one's rounds
 };
 
 // Opaque multipliers of the FMA-pipe forms (kernel parameter: ptxas cannot
@@ -342,6 +344,9 @@ t3_sp_kernel(const uint2* in, uint2* out, uint64_t nblocks, const uint32_t* __re
     // one global round trip: every thread issues its few loads together, then
     // the 32-fold lane replication is a shared-memory copy (a fill loop of 64
     // dependent-latency global loads per thread cost ~7 us per launch)
+    const uint64_t b0 = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    uint2 vnext = make_uint2(0u, 0u);
+    if ((SPV & T3_SPV_PREFETCH) && b0 < nblocks) vnext = __ldcs(in + b0);  // overlaps the fill
     if (!(SPV & T3_SPV_KEYPARAM))
         for (int w = threadIdx.x; w < int(sizeof(T3SpKeyParam) / 4); w += blockDim.x) ks[w] = __ldg(keys_global + w);
     const uint32_t* ks2 = ks + 48 * 8;  // T3SpKeyParam::k2
@@ -353,8 +358,14 @@ t3_sp_kernel(const uint2* in, uint2* out, uint64_t nblocks, const uint32_t* __re
     const char* smem = reinterpret_cast<const char*>(t3_sp_smem);
     const uint32_t lane4 = (threadIdx.x & 31) * 4;
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-    for (uint64_t b = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < nblocks; b += stride) {
-        const uint2 v = __ldcs(in + b);
+    for (uint64_t b = b0; b < nblocks; b += stride) {
+        uint2 v;
+        if (SPV & T3_SPV_PREFETCH) {
+            v = vnext;
+            if (b + stride < nblocks) vnext = __ldcs(in + b + stride);  // read before any write: in place is safe
+        } else {
+            v = __ldcs(in + b);
+        }
         uint32_t x = __byte_perm(v.x, 0, 0x0123);  // big-endian high word
         uint32_t y = __byte_perm(v.y, 0, 0x0123);
         // IP as five delta swaps (verified against the FIPS table in tests).

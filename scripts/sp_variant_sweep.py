@@ -10,7 +10,7 @@ import torch  # noqa: E402
 import paper_1305_4376_b200 as t3  # noqa: E402
 
 KEY = "133457799BBCDFF10E329232EA6D0D737CA110454A1A6E57"
-masks = [int(a) for a in sys.argv[1:]] or [0, 106]
+masks = [int(a) for a in sys.argv[1:]] or [0, 234]
 wgs = [int(w) for w in os.environ.get("SP_WG", "0").split(",")]
 masks = [(m, w) for m in masks for w in wgs]
 s = torch.cuda.current_stream().cuda_stream

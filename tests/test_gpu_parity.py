@@ -105,10 +105,10 @@ def test_chunk_and_work_group_invariance(eng, oracle):
             assert np.array_equal(run(eng, ts, x, 0, N.VARIANT_SPTABLE, chunk=chunk, wg=wg), want)
 
 
-@pytest.mark.parametrize("spv", [0, 106])
+@pytest.mark.parametrize("spv", [0, 234])
 def test_sptable_codegen_masks_and_cta_sizes(oracle, spv, monkeypatch):
     """SP-table kernel: the previous round structure (mask 0) and the shipped
-    one (106: key XOR on R, uniform keys, FMA merges), 256- and 1024-thread
+    one (234: key XOR on R, uniform keys, FMA merges, prefetch), 256- and 1024-thread
     CTAs (the size rule switches at 16384 blocks) and explicit work groups up
     to 1024, all keying options, both directions, against the oracle."""
     monkeypatch.setenv("T3DES_SP_VAR", str(spv))  # read at context creation
