@@ -128,6 +128,31 @@ def test_sptable_codegen_masks_and_cta_sizes(oracle, spv, monkeypatch):
         e.close()
 
 
+def test_rekey_between_async_launches(eng, oracle):
+    """set_schedule no longer synchronises the device (tables travel by value
+    as kernel parameters): a launch in flight keeps its own key while the
+    next launch, queued right behind it, uses the new one — for both
+    kernels and both stream orders."""
+    st = torch.cuda.Stream()
+    n = 300_001  # several waves of the bitsliced kernel + a tail
+    x = np.random.default_rng(7).integers(0, 256, 8 * n, dtype=np.uint8)
+    small = x[: 8 * 4099]
+    for variant in (N.VARIANT_BITSLICE, N.VARIANT_SPTABLE, N.VARIANT_AUTO):
+        eng.set_variant(variant)
+        eng.set_launch(0, 0)
+        outs = []
+        with torch.cuda.stream(st):
+            for k, (keyhex, data) in enumerate([(KEYS[0], x), (KEYS[1], small), (KEYS[2], x), (KEYS[0], small)]):
+                eng.set_schedule(t3.triple_schedule(t3.parse_hex_key(keyhex)))
+                src = dev(data)
+                dst = torch.empty_like(src)
+                eng.ecb_device(k % 2, src.data_ptr(), dst.data_ptr(), data.nbytes, st.cuda_stream)
+                outs.append((keyhex, data, k % 2, src, dst))
+        st.synchronize()
+        for keyhex, data, d, _, dst in outs:
+            assert np.array_equal(host(dst), oracle.ecb(data, oracle.schedule_hex(keyhex), d)), (variant, keyhex)
+
+
 def test_device_errors(eng):
     ts = t3.triple_schedule(t3.parse_hex_key(KEYS[0]))
     eng.set_schedule(ts)
