@@ -30,6 +30,20 @@ __global__ void __launch_bounds__(256) k(uint32_t* out, int iters, uint32_t cval
                 else asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[i]) : "r"(y), "r"(z));
             }
             if (FORM == 8) asm volatile("lop3.b32 %0, %0, %1, 0, 0x3C;" : "+r"(x[i]) : "r"(y));  // 2-input xor
+            if (FORM == 9) asm volatile("mul.hi.u32 %0, %0, %1;" : "+r"(x[i]) : "r"(cval));  // IMAD.HI
+            if (FORM == 10) {  // IMAD.WIDE: 64-bit product, both halves kept live
+                uint64_t w;
+                asm volatile("mul.wide.u32 %0, %1, %2;" : "=l"(w) : "r"(x[i]), "r"(cval));
+                x[i] = uint32_t(w) ^ uint32_t(w >> 32);
+            }
+            if (FORM == 11) {  // LOP3 and IMAD.HI interleaved 1:1
+                if (i & 1) asm volatile("mul.hi.u32 %0, %0, %1;" : "+r"(x[i]) : "r"(cval));
+                else asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[i]) : "r"(y), "r"(z));
+            }
+            if (FORM == 12) {  // LOP3 : IMAD.SHL-style mad by a register power of two, 1:1
+                if (i & 1) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(x[i]) : "r"(cval), "r"(z));
+                else asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[i]) : "r"(y), "r"(z));
+            }
         }
     }
     uint32_t s = 0;
@@ -73,5 +87,8 @@ int main() {
     run<5>("IMAD R,R,c[],R (param)", d, p.multiProcessorCount, clk);
     run<6>("LOP3 + IMAD 1:1", d, p.multiProcessorCount, clk);
     run<7>("LOP3 + IMAD 3:1", d, p.multiProcessorCount, clk);
+    run<9>("IMAD.HI R,R,R (mul.hi)", d, p.multiProcessorCount, clk);
+    run<10>("IMAD.WIDE R,R,R (+lop3 fold)", d, p.multiProcessorCount, clk);
+    run<11>("LOP3 + IMAD.HI 1:1", d, p.multiProcessorCount, clk);
     return 0;
 }
