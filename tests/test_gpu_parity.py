@@ -167,6 +167,30 @@ def test_device_errors(eng):
     fresh.close()
 
 
+@pytest.mark.parametrize("nbytes", [8, 8 * 1023, 512 << 10, (512 << 10) + 8, (2 << 20) + 8, (8 << 20) + 24,
+                                    (20 << 20) + 8 * 517])
+def test_host_path_small_batch_stages(eng, oracle, nbytes):
+    """t3des_cu_ecb_host below 64 MiB: the stage size adapts (whole batch,
+    then 2, 4, 8 stages with ragged last stages); pageable and pinned spans,
+    in place and out of place, byte-exact against the oracle."""
+    ts = t3.triple_schedule(t3.parse_hex_key(KEYS[1]))
+    s = oracle.schedule_hex(KEYS[1])
+    eng.set_schedule(ts)
+    eng.set_variant(N.VARIANT_AUTO)
+    eng.set_launch(0, 0)
+    x = np.random.default_rng(nbytes).integers(0, 256, nbytes, dtype=np.uint8)
+    want = oracle.ecb(x, s, 0)
+    y = np.zeros_like(x)
+    eng.ecb_host(0, x.ctypes.data, y.ctypes.data, nbytes)  # pageable -> pageable
+    assert np.array_equal(y, want)
+    pinned = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    pinned.numpy()[:] = x
+    eng.ecb_host(0, pinned.data_ptr(), pinned.data_ptr(), nbytes)  # pinned, in place
+    assert np.array_equal(pinned.numpy(), want)
+    eng.ecb_host(1, pinned.data_ptr(), y.ctypes.data, nbytes)  # pinned -> pageable
+    assert np.array_equal(y, x)
+
+
 def test_host_path_pipeline(eng, oracle):
     """t3des_cu_ecb_host: >64 MiB to cross several pipeline chunks, pageable
     and pinned buffers, in place."""
