@@ -23,7 +23,7 @@
 
 namespace {
 
-constexpr std::uint64_t kSpBigCtaMinBlocks = 16384;  // 128 KiB
+constexpr std::uint64_t kSpMinThreads = 128;  // SP-table CTA size floor for small batches
 constexpr int kSpSmemBytes = 8 * 64 * 32 * 4 + int(sizeof(T3SpKeyParam)) + 8 * 64 * 4;  // 64 KiB tables, round keys, staging
 
 // Restores the caller's current device on scope exit.
@@ -172,18 +172,20 @@ T3SpMul sp_mul() {
 int launch_sptable(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8_t* out,
                    std::uint64_t nblocks, cudaStream_t s) {
     // CTA size: 1024 threads (2 CTAs = 64 warps per SM, and the 64 KiB table
-    // fill split 4x finer) unless the batch is too small to give every SM a
-    // CTA, where 256-thread CTAs spread it wider (scripts/sp_variant_sweep.py:
-    // 1 GiB 160 vs 140 GB/s; 8 KiB 8.2 vs 12.4 us)
-    const int threads = c->work_group > 0                     ? c->work_group
-                        : nblocks >= kSpBigCtaMinBlocks       ? T3_SP_THREADS_BIG
-                                                              : T3_SP_THREADS;
+    // fill split 4x finer: 1 GiB 160 vs 140 GB/s with 256) once every SM gets
+    // a full CTA; below that one CTA per SM with just enough threads, so a
+    // small batch spreads over all SMs (scripts/sp_variant_sweep.py).
+    const std::uint64_t per_sm = (nblocks + c->sms - 1) / std::uint64_t(c->sms);
+    const int threads = c->work_group > 0 ? c->work_group
+                        : per_sm >= std::uint64_t(T3_SP_THREADS_BIG)
+                            ? T3_SP_THREADS_BIG
+                            : int(std::max<std::uint64_t>(kSpMinThreads, (per_sm + 31) / 32 * 32));
     std::uint64_t grid = (nblocks + threads - 1) / threads;
     int occ = threads == T3_SP_THREADS ? c->sp_occ : threads == T3_SP_THREADS_BIG ? c->sp_occ_big : 0;
-    if (!occ &&
+    if (!occ && grid > std::uint64_t(c->sms) &&
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sp_kernel_fn(c->sp_var), threads, kSpSmemBytes) != cudaSuccess)
         return T3DES_CU_ERR_CUDA;
-    grid = std::min<std::uint64_t>(grid, std::uint64_t(c->sms) * std::uint64_t(std::max(occ, 1)));
+    if (occ) grid = std::min<std::uint64_t>(grid, std::uint64_t(c->sms) * std::uint64_t(occ));
     const bool single = c->rounds == 16;
     const auto* sin = reinterpret_cast<const uint2*>(in);
     auto* sout = reinterpret_cast<uint2*>(out);

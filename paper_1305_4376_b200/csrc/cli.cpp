@@ -340,9 +340,14 @@ int run_bench(const Opts& o) {
         if (o.sweep == "workers") r.workers = static_cast<unsigned>(v);
         if (o.sweep == "chunk") r.chunk = v;
         if (o.sweep == "workgroup") r.wg = v;
-        if (r.wg == 0) {  // the kernels' own CTA sizes (capi.cu launch_sptable / launch_bitslice)
+        const std::size_t wg_arg = r.wg;  // 0 = the kernels' own CTA-size rule
+        if (r.wg == 0) {  // report the size that rule picks (capi.cu launch_sptable / launch_bitslice)
             const std::uint64_t launch_blocks = r.chunk ? std::min<std::uint64_t>(r.chunk, bytes / 8) : bytes / 8;
-            r.wg = o.variant == "sptable" ? (launch_blocks >= 16384 ? 1024 : 256) : 128;
+            int sms = 148;
+            if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, o.device) != cudaSuccess) sms = 148;
+            const std::uint64_t per_sm = (launch_blocks + sms - 1) / std::uint64_t(sms);
+            r.wg = o.variant == "sptable" ? (per_sm >= 1024 ? 1024 : std::max<std::uint64_t>(128, (per_sm + 31) / 32 * 32))
+                                          : 128;
         }
         try {
             double best = 0;
@@ -356,7 +361,7 @@ int run_bench(const Opts& o) {
                 cudaMemcpy(din, payload.data(), bytes, cudaMemcpyHostToDevice);
                 rc = t3des_cu_set_schedule(c, sub48);
                 if (!rc) rc = t3des_cu_set_variant(c, make_config(o).variant);
-                if (!rc) rc = t3des_cu_set_launch(c, r.chunk, static_cast<int>(r.wg));
+                if (!rc) rc = t3des_cu_set_launch(c, r.chunk, static_cast<int>(wg_arg));
                 cudaEvent_t e0, e1;
                 cudaEventCreate(&e0);
                 cudaEventCreate(&e1);
@@ -380,7 +385,7 @@ int run_bench(const Opts& o) {
                 t3des::DispatchConfig cfg = make_config(o);
                 cfg.workers = r.workers;
                 cfg.chunk_blocks = r.chunk;
-                cfg.work_group = r.wg;
+                cfg.work_group = wg_arg;
                 cfg.gpu_chunked = true;
                 for (unsigned rep = 0; rep <= o.reps; ++rep) {
                     const auto t0 = std::chrono::steady_clock::now();

@@ -352,8 +352,13 @@ t3_sp_kernel(const uint2* in, uint2* out, uint64_t nblocks, const uint32_t* __re
     const uint32_t* ks2 = ks + 48 * 8;  // T3SpKeyParam::k2
     for (int w = threadIdx.x; w < 8 * 64; w += blockDim.x) sp[w] = __ldg(sp_global + w);
     __syncthreads();
-#pragma unroll 8
-    for (int w = threadIdx.x; w < 8 * 64 * 32; w += blockDim.x) t3_sp_smem[w] = sp[w >> 5];
+    // lane replication: each table word fills 32 consecutive words (8 x 16 B)
+    uint4* fill = reinterpret_cast<uint4*>(t3_sp_smem);
+#pragma unroll 4
+    for (int w = threadIdx.x; w < 8 * 64 * 8; w += blockDim.x) {
+        const uint32_t v = sp[w >> 3];
+        fill[w] = make_uint4(v, v, v, v);
+    }
     __syncthreads();
     const char* smem = reinterpret_cast<const char*>(t3_sp_smem);
     const uint32_t lane4 = (threadIdx.x & 31) * 4;
