@@ -186,6 +186,12 @@ class Engine:
         _raise(self._lib.t3des_cu_create(int(device), ctypes.byref(h)), f"device {device}")
         self._h = h
         self.device = int(device)
+        # last values installed through this wrapper: the batch API re-applies
+        # schedule / variant / launch shape on every call, and skipping the
+        # unchanged ones saves the ctypes round trips (TripleSchedule is frozen)
+        self._ts = None
+        self._variant = None
+        self._launch = None
 
     def close(self) -> None:
         if getattr(self, "_h", None):
@@ -199,13 +205,29 @@ class Engine:
             pass
 
     def set_schedule(self, ts: TripleSchedule) -> None:
+        if ts is self._ts:
+            return
+        self._ts = None
         _raise(self._lib.t3des_cu_set_schedule(self._h, ts.sub48()))
+        self._ts = ts
+
+    def set_sub48(self, sub48) -> None:
+        """Install a raw pass-major 48-subkey array (ctypes c_uint64 * 48)."""
+        self._ts = None
+        _raise(self._lib.t3des_cu_set_schedule(self._h, sub48))
 
     def set_variant(self, variant: int) -> None:
+        if variant == self._variant:
+            return
         _raise(self._lib.t3des_cu_set_variant(self._h, int(variant)))
+        self._variant = int(variant)
 
     def set_launch(self, chunk_blocks: int = 0, work_group: int = 0) -> None:
-        _raise(self._lib.t3des_cu_set_launch(self._h, int(chunk_blocks), int(work_group)))
+        shape = (int(chunk_blocks), int(work_group))
+        if shape == self._launch:
+            return
+        _raise(self._lib.t3des_cu_set_launch(self._h, *shape))
+        self._launch = shape
 
     def set_pipeline(self, chunk_bytes: int = 32 << 20, streams: int = 3) -> None:
         _raise(self._lib.t3des_cu_set_pipeline(self._h, int(chunk_bytes), int(streams)))

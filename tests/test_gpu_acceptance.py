@@ -23,7 +23,7 @@ def eng(engine_lib):
 
 
 def _run(eng, sub48, x, d, variant=N.VARIANT_AUTO):
-    eng._lib.t3des_cu_set_schedule(eng._h, sub48)
+    eng.set_sub48(sub48)
     eng.set_variant(variant)
     src = torch.from_numpy(x).cuda()
     dst = torch.empty_like(src)
