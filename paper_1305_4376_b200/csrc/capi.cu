@@ -24,6 +24,8 @@
 namespace {
 
 constexpr std::uint64_t kSpMinThreads = 128;  // SP-table CTA size floor for small batches
+// pinned host batches up to this size run zero-copy (kernel on the mapped pages)
+constexpr std::size_t kZeroCopyMaxBytes = std::size_t(1) << 20;  // scripts/zerocopy_sweep.py
 constexpr int kSpSmemBytes = 8 * 64 * 32 * 4 + int(sizeof(T3SpKeyParam)) + 8 * 64 * 4;  // 64 KiB tables, round keys, staging
 
 // Restores the caller's current device on scope exit.
@@ -293,6 +295,26 @@ int ensure_staging(t3des_cu_ctx* c, std::size_t bytes, int n) {
     for (int i = 0; i < n; ++i) T3_CK(cudaMalloc(&c->buf[i], bytes));
     c->buf_bytes = bytes;
     return T3DES_CU_OK;
+}
+
+// What a host-span pointer is, from one attribute query: device-only memory
+// (not a valid host span), page-locked host memory, and the device address
+// under which page-locked memory is mapped (null if it is not mapped).
+struct SpanKind {
+    bool device_only = false, pinned = false;
+    void* mapped = nullptr;
+};
+SpanKind classify_span(const void* p) {
+    SpanKind k;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return k;
+    }
+    k.device_only = a.type == cudaMemoryTypeDevice;
+    k.pinned = a.type == cudaMemoryTypeHost;
+    if (k.pinned) k.mapped = a.devicePointer;
+    return k;
 }
 
 // Page-locked (cudaMallocHost / cudaHostRegister) host memory?
@@ -649,9 +671,24 @@ int t3des_cu_ecb_host(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uin
     if (rc) return rc;
     if (!len) return T3DES_CU_OK;
     DeviceScope scope(c->device);
-    if (t3b::device_only(in) || t3b::device_only(out)) return T3DES_CU_ERR_ARG;  // use t3des_cu_ecb_device
-    const bool in_pinned = t3b::host_pinned(in), out_pinned = t3b::host_pinned(out);
-    if (!in_pinned || !out_pinned) return t3b::ecb_host_staged(c, dir, in, out, len, in_pinned, out_pinned);
+    const t3b::SpanKind ki = t3b::classify_span(in), ko = in == out ? ki : t3b::classify_span(out);
+    if (ki.device_only || ko.device_only) return T3DES_CU_ERR_ARG;  // use t3des_cu_ecb_device
+    if (!ki.pinned || !ko.pinned) return t3b::ecb_host_staged(c, dir, in, out, len, ki.pinned, ko.pinned);
+    // Small pinned batches: the SP-table kernel reads and writes the mapped
+    // host pages directly over PCIe — no DMA setup in either direction.
+    std::size_t zc_max = kZeroCopyMaxBytes;
+    if (const char* e = std::getenv("T3DES_ZEROCOPY_MAX")) zc_max = std::strtoull(e, nullptr, 10);
+    if (len <= zc_max && ki.mapped && ko.mapped && !c->chunk_blocks &&
+        ((reinterpret_cast<std::uintptr_t>(ki.mapped) | reinterpret_cast<std::uintptr_t>(ko.mapped)) & 7u) == 0 &&
+        (c->variant == T3DES_CU_VARIANT_AUTO || c->variant == T3DES_CU_VARIANT_SPTABLE) &&
+        len / 8 <= T3DES_CU_AUTO_SMALL_BLOCKS) {
+        cudaStream_t s = c->st[0];
+        if (int rc2 = launch_sptable(c, dir, static_cast<const std::uint8_t*>(ki.mapped),
+                                     static_cast<std::uint8_t*>(ko.mapped), len / 8, s))
+            return rc2;
+        T3_CK(cudaStreamSynchronize(s));
+        return T3DES_CU_OK;
+    }
     // Stage size: as set, or adapted to the batch — about 8 stages, between
     // 8 and 32 MiB (scripts/e2e_size_sweep.py: 32-64 MiB batches gain ~10-30%
     // from 8 MiB stages, >= 256 MiB batches prefer 32 MiB), whole tiles.
