@@ -25,7 +25,7 @@ namespace {
 
 constexpr std::uint64_t kSpMinThreads = 128;  // SP-table CTA size floor for small batches
 // pinned host batches up to this size run zero-copy (kernel on the mapped pages)
-constexpr std::size_t kZeroCopyMaxBytes = std::size_t(1) << 20;  // scripts/zerocopy_sweep.py
+constexpr std::size_t kZeroCopyMaxBytes = std::size_t(64) << 20;  // scripts/zerocopy_{sweep,big}.py
 constexpr int kSpSmemBytes = 8 * 64 * 32 * 4 + int(sizeof(T3SpKeyParam)) + 8 * 64 * 4;  // 64 KiB tables, round keys, staging
 
 // Restores the caller's current device on scope exit.
@@ -674,14 +674,15 @@ int t3des_cu_ecb_host(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uin
     const t3b::SpanKind ki = t3b::classify_span(in), ko = in == out ? ki : t3b::classify_span(out);
     if (ki.device_only || ko.device_only) return T3DES_CU_ERR_ARG;  // use t3des_cu_ecb_device
     if (!ki.pinned || !ko.pinned) return t3b::ecb_host_staged(c, dir, in, out, len, ki.pinned, ko.pinned);
-    // Small pinned batches: the SP-table kernel reads and writes the mapped
-    // host pages directly over PCIe — no DMA setup in either direction.
+    // Pinned batches up to 64 MiB: the SP-table kernel reads and writes the
+    // mapped host pages directly over PCIe — no DMA setup in either direction,
+    // and the kernel (~158 GB/s) stays far ahead of the link.  Larger batches
+    // reach more of the link through the copy engines (DMA pipeline below).
     std::size_t zc_max = kZeroCopyMaxBytes;
-    if (const char* e = std::getenv("T3DES_ZEROCOPY_MAX")) zc_max = std::strtoull(e, nullptr, 10);
+    if (const char* e = std::getenv("T3DES_ZEROCOPY_MAX")) zc_max = std::strtoull(e, nullptr, 10);  // experiments
     if (len <= zc_max && ki.mapped && ko.mapped && !c->chunk_blocks &&
         ((reinterpret_cast<std::uintptr_t>(ki.mapped) | reinterpret_cast<std::uintptr_t>(ko.mapped)) & 7u) == 0 &&
-        (c->variant == T3DES_CU_VARIANT_AUTO || c->variant == T3DES_CU_VARIANT_SPTABLE) &&
-        len / 8 <= T3DES_CU_AUTO_SMALL_BLOCKS) {
+        (c->variant == T3DES_CU_VARIANT_AUTO || c->variant == T3DES_CU_VARIANT_SPTABLE)) {
         cudaStream_t s = c->st[0];
         if (int rc2 = launch_sptable(c, dir, static_cast<const std::uint8_t*>(ki.mapped),
                                      static_cast<std::uint8_t*>(ko.mapped), len / 8, s))
