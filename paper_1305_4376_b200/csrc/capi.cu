@@ -378,6 +378,25 @@ int ecb_host_staged(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8
         c->pool_out = new t3b::CopyPool(std::max(1, total / 2));
     }
     const std::size_t nst = (len + S - 1) / S;
+    // One small stage between two pageable spans: copy in, run the SP-table
+    // kernel zero-copy on the mapped pinned slot, copy out (no DMA setups).
+    if (nst == 1 && !in_pinned && !out_pinned && !c->chunk_blocks &&
+        (c->variant == T3DES_CU_VARIANT_AUTO || c->variant == T3DES_CU_VARIANT_SPTABLE)) {
+        std::uint8_t* h = c->hbuf[0];
+        void* d = nullptr;
+        T3_CK(cudaHostGetDevicePointer(&d, h, 0));
+        c->pool_in->start(h, in, len);
+        c->pool_in->wait();
+        int rc0 = launch_sptable(c, dir, static_cast<std::uint8_t*>(d), static_cast<std::uint8_t*>(d), len / 8, c->st[0]);
+        if (!rc0 && cudaStreamSynchronize(c->st[0]) != cudaSuccess) rc0 = T3DES_CU_ERR_CUDA;
+        if (rc0) {
+            (void)cudaGetLastError();
+            return rc0;
+        }
+        c->pool_out->start(out, h, len);
+        c->pool_out->wait();
+        return T3DES_CU_OK;
+    }
     auto off = [&](std::size_t k) { return k * S; };
     auto cnt = [&](std::size_t k) { return std::min(S, len - k * S); };
     // Errors never return with a copy job in flight (the pools would keep
