@@ -26,6 +26,8 @@ namespace {
 constexpr std::uint64_t kSpMinThreads = 128;  // SP-table CTA size floor for small batches
 // pinned host batches up to this size run zero-copy (kernel on the mapped pages)
 constexpr std::size_t kZeroCopyMaxBytes = std::size_t(64) << 20;  // scripts/zerocopy_{sweep,big}.py
+// pageable batches up to this size run their stages zero-copy on the pinned slots
+constexpr std::size_t kStagedZeroCopyMaxBytes = std::size_t(12) << 20;
 constexpr int kSpSmemBytes = 8 * 64 * 32 * 4 + int(sizeof(T3SpKeyParam)) + 8 * 64 * 4;  // 64 KiB tables, round keys, staging
 
 // Restores the caller's current device on scope exit.
@@ -399,6 +401,14 @@ int ecb_host_staged(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8
     }
     auto off = [&](std::size_t k) { return k * S; };
     auto cnt = [&](std::size_t k) { return std::min(S, len - k * S); };
+    // pageable on both sides and at most 12 MiB: stages run zero-copy on their
+    // mapped pinned slots (no DMA); above that the host copies and the kernel's
+    // PCIe traffic contend and the DMA pipeline is as fast or faster
+    // (scripts/zerocopy_big.py with ZC_PAGEABLE=1, profiles/r1/zerocopy_r1n.txt)
+    std::size_t zc_max = kStagedZeroCopyMaxBytes;
+    if (const char* e = std::getenv("T3DES_ZEROCOPY_MAX")) zc_max = std::strtoull(e, nullptr, 10);  // experiments
+    const bool zc = !in_pinned && !out_pinned && len <= zc_max && !c->chunk_blocks &&
+                    (c->variant == T3DES_CU_VARIANT_AUTO || c->variant == T3DES_CU_VARIANT_SPTABLE);
     // Errors never return with a copy job in flight (the pools would keep
     // writing into the caller's buffers): every started job is waited for.
     int rc = T3DES_CU_OK;
@@ -426,10 +436,16 @@ int ecb_host_staged(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8
             const std::uint8_t* src = in_pinned ? in + off(k) : c->hbuf[slot];
             std::uint8_t* dst = out_pinned ? out + off(k) : c->hbuf[slot];
             const std::size_t n = cnt(k);
-            if (cudaMemcpyAsync(c->hdev[slot], src, n, cudaMemcpyHostToDevice, s) != cudaSuccess) rc = T3DES_CU_ERR_CUDA;
-            if (!rc) rc = run_device(c, dir, c->hdev[slot], c->hdev[slot], n / 8, s);
-            if (!rc && cudaMemcpyAsync(dst, c->hdev[slot], n, cudaMemcpyDeviceToHost, s) != cudaSuccess)
-                rc = T3DES_CU_ERR_CUDA;
+            if (zc) {  // the SP-table kernel on the mapped pinned slot
+                void* d = nullptr;
+                if (cudaHostGetDevicePointer(&d, c->hbuf[slot], 0) != cudaSuccess) rc = T3DES_CU_ERR_CUDA;
+                if (!rc) rc = launch_sptable(c, dir, static_cast<std::uint8_t*>(d), static_cast<std::uint8_t*>(d), n / 8, s);
+            } else {
+                if (cudaMemcpyAsync(c->hdev[slot], src, n, cudaMemcpyHostToDevice, s) != cudaSuccess) rc = T3DES_CU_ERR_CUDA;
+                if (!rc) rc = run_device(c, dir, c->hdev[slot], c->hdev[slot], n / 8, s);
+                if (!rc && cudaMemcpyAsync(dst, c->hdev[slot], n, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+                    rc = T3DES_CU_ERR_CUDA;
+            }
             if (!rc && cudaEventRecord(c->hev[slot], s) != cudaSuccess) rc = T3DES_CU_ERR_CUDA;
             c->hev_live[slot] = !rc;
         }
