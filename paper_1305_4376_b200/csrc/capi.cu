@@ -299,13 +299,6 @@ int ensure_staging(t3des_cu_ctx* c, std::size_t bytes, int n) {
     return T3DES_CU_OK;
 }
 
-// What a host-span pointer is, from one attribute query: device-only memory
-// (not a valid host span), page-locked host memory, and the device address
-// under which page-locked memory is mapped (null if it is not mapped).
-struct SpanKind {
-    bool device_only = false, pinned = false;
-    void* mapped = nullptr;
-};
 SpanKind classify_span(const void* p) {
     SpanKind k;
     cudaPointerAttributes a;
@@ -317,26 +310,6 @@ SpanKind classify_span(const void* p) {
     k.pinned = a.type == cudaMemoryTypeHost;
     if (k.pinned) k.mapped = a.devicePointer;
     return k;
-}
-
-// Page-locked (cudaMallocHost / cudaHostRegister) host memory?
-bool host_pinned(const void* p) {
-    cudaPointerAttributes a;
-    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-        (void)cudaGetLastError();
-        return false;
-    }
-    return a.type == cudaMemoryTypeHost;
-}
-
-// Device memory (not host-accessible): not a valid host span.
-bool device_only(const void* p) {
-    cudaPointerAttributes a;
-    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-        (void)cudaGetLastError();
-        return false;
-    }
-    return a.type == cudaMemoryTypeDevice;
 }
 
 // Pageable spans (hoststage.hpp): stage k goes through pinned slot k % R and

@@ -74,11 +74,15 @@ int run_device(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8_t* o
 // Make sure the first n staging buffers hold at least `bytes` each.
 int ensure_staging(t3des_cu_ctx* c, std::size_t bytes, int n);
 
-// Page-locked host memory (DMA-able without bouncing)?
-bool host_pinned(const void* p);
-
-// Device-only memory (an error for the host entry points)?
-bool device_only(const void* p);
+// What a host-span pointer is, from one attribute query: device-only memory
+// (an error for the host entry points), page-locked host memory (DMA-able
+// without bouncing), and the device address under which page-locked memory
+// is mapped (null if it is not mapped for the current device).
+struct SpanKind {
+    bool device_only = false, pinned = false;
+    void* mapped = nullptr;
+};
+SpanKind classify_span(const void* p);
 
 // t3des_cu_ecb_host for spans that are not both pinned: pinned ring staging
 // with host copy threads (hoststage.hpp).
