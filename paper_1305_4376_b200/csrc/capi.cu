@@ -28,6 +28,8 @@ constexpr std::uint64_t kSpMinThreads = 128;  // SP-table CTA size floor for sma
 constexpr std::size_t kZeroCopyMaxBytes = std::size_t(64) << 20;  // scripts/zerocopy_{sweep,big}.py
 // pageable batches up to this size run their stages zero-copy on the pinned slots
 constexpr std::size_t kStagedZeroCopyMaxBytes = std::size_t(12) << 20;
+// first/last stage size of the pinned DMA pipeline's ramp (large batches)
+constexpr std::size_t kRampBytes = std::size_t(8) << 20;  // scripts/ramp_sweep.py
 constexpr int kSpSmemBytes = 8 * 64 * 32 * 4 + int(sizeof(T3SpKeyParam)) + 8 * 64 * 4;  // 64 KiB tables, round keys, staging
 
 // Restores the caller's current device on scope exit.
@@ -714,9 +716,26 @@ int t3des_cu_ecb_host(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uin
     // Stage k: H2D, kernel, D2H on stream k % ns (in-order per stream, so a
     // stream's buffer is free again when its next stage starts); stages on
     // different streams overlap copies in both directions with kernels.
+    // Ramp (large batches, default shape): the first stages grow from
+    // kRampBytes to `chunk` and the last ones shrink back, so the pipeline
+    // fills and drains in small steps instead of one full stage each way.
+    std::size_t ramp = 0;
+    if (!c->pipe_explicit && len >= (std::size_t(64) << 20)) ramp = kRampBytes;
+    if (const char* e = std::getenv("T3DES_RAMP_KIB")) ramp = std::size_t(std::atoi(e)) << 10;  // experiments
+    auto stage_bytes = [&](std::size_t k, std::size_t left) {
+        std::size_t n = std::min(chunk, left);
+        if (ramp && ramp < chunk) {
+            if (k < 16) n = std::min(n, ramp << k);
+            if (left < 2 * chunk && left > ramp) {  // tail: halve towards the ramp size
+                std::size_t h = (left / 2 + 8 * T3_TILE_BLOCKS - 1) / (8 * T3_TILE_BLOCKS) * (8 * T3_TILE_BLOCKS);
+                n = std::min(n, std::max(h, ramp));
+            }
+        }
+        return n;
+    };
     std::size_t k = 0;
-    for (std::size_t off = 0; off < len; off += chunk, ++k) {
-        const std::size_t n = std::min(chunk, len - off);
+    for (std::size_t off = 0, n = 0; off < len; off += n, ++k) {
+        n = stage_bytes(k, len - off);
         cudaStream_t s = c->st[k % ns];
         std::uint8_t* b = c->buf[k % ns];
         T3_CK(cudaMemcpyAsync(b, in + off, n, cudaMemcpyHostToDevice, s));
