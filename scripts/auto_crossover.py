@@ -1,3 +1,6 @@
+#!/usr/bin/env python3
+"""Per-launch time of the bitsliced and SP-table kernels around the AUTO
+threshold (1-3 MiB), 200 launches each."""
 import os, sys
 sys.path.insert(0, os.getcwd())
 import torch

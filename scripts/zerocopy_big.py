@@ -1,3 +1,7 @@
+#!/usr/bin/env python3
+"""Host batches through t3des_cu_ecb_host: DMA pipeline (AUTO) vs zero-copy
+with the SP-table kernel on mapped pages, GB/s end to end; pinned buffers, or
+pageable ones with ZC_PAGEABLE=1.  Usage: zerocopy_big.py [MiB ...]"""
 import os, sys, time
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch
