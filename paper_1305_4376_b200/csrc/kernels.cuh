@@ -237,6 +237,8 @@ enum : int {
                           // the lane column then merges into the mask lop3
     T3_SPV_PREFETCH = 128, // a thread's first block loaded before the table fill, each next
                            // block before the current one's rounds
+    T3_SPV_PDL = 256,      // programmatic dependent launch: the table fill overlaps the previous
+                           // kernel on the stream; input is touched only after griddepcontrol.wait
 };
 
 // Opaque multipliers of the FMA-pipe forms (kernel parameter: ptxas cannot
@@ -337,16 +339,19 @@ template <int SPV>
 __global__ void __launch_bounds__(1024)
 t3_sp_kernel(const uint2* in, uint2* out, uint64_t nblocks, const uint32_t* __restrict__ sp_global,
              int passes, const uint32_t* __restrict__ keys_global, const __grid_constant__ T3SpMul mul,
-             const __grid_constant__ T3SpKeyParam kp) {
+             const __grid_constant__ T3SpKeyParam kp, int pdl) {
     extern __shared__ __align__(16) uint32_t t3_sp_smem[];
     uint32_t* ks = t3_sp_smem + 8 * 64 * 32;  // [48][8]
     uint32_t* sp = ks + sizeof(T3SpKeyParam) / 4;  // the 2 KiB table, staged once
     // one global round trip: every thread issues its few loads together, then
     // the 32-fold lane replication is a shared-memory copy (a fill loop of 64
     // dependent-latency global loads per thread cost ~7 us per launch)
+    if (SPV & T3_SPV_PDL) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const uint64_t b0 = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     uint2 vnext = make_uint2(0u, 0u);
-    if ((SPV & T3_SPV_PREFETCH) && b0 < nblocks) vnext = __ldcs(in + b0);  // overlaps the fill
+    // pdl: launched with programmatic serialisation (host decides per launch);
+    // the input may still be being written by the previous kernel until the wait
+    if ((SPV & T3_SPV_PREFETCH) && !pdl && b0 < nblocks) vnext = __ldcs(in + b0);  // overlaps the fill
     if (!(SPV & T3_SPV_KEYPARAM))
         for (int w = threadIdx.x; w < int(sizeof(T3SpKeyParam) / 4); w += blockDim.x) ks[w] = __ldg(keys_global + w);
     const uint32_t* ks2 = ks + 48 * 8;  // T3SpKeyParam::k2
@@ -360,6 +365,10 @@ t3_sp_kernel(const uint2* in, uint2* out, uint64_t nblocks, const uint32_t* __re
         fill[w] = make_uint4(v, v, v, v);
     }
     __syncthreads();
+    if ((SPV & T3_SPV_PDL) && pdl) {  // the previous grid on the stream has completed from here on
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        if ((SPV & T3_SPV_PREFETCH) && b0 < nblocks) vnext = __ldcs(in + b0);
+    }
     const char* smem = reinterpret_cast<const char*>(t3_sp_smem);
     const uint32_t lane4 = (threadIdx.x & 31) * 4;
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;

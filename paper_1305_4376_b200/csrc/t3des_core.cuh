@@ -134,7 +134,7 @@ struct T3SpKeyParam {
 };
 
 #ifndef T3_SPV_DEFAULT
-#define T3_SPV_DEFAULT 234  // T3_SPV_* mask of the SP-table kernel (kernels.cuh): KEY2|KEYPARAM|SHLFMA|MERGE6|PREFETCH
+#define T3_SPV_DEFAULT 490  // T3_SPV_* mask of the SP-table kernel (kernels.cuh): KEY2|KEYPARAM|SHLFMA|MERGE6|PREFETCH|PDL
 #endif
 
 // In-register transpose of a 32x32 bit matrix: afterwards x[k] bit m is the

@@ -105,10 +105,10 @@ def test_chunk_and_work_group_invariance(eng, oracle):
             assert np.array_equal(run(eng, ts, x, 0, N.VARIANT_SPTABLE, chunk=chunk, wg=wg), want)
 
 
-@pytest.mark.parametrize("spv", [0, 234])
+@pytest.mark.parametrize("spv", [0, 490])
 def test_sptable_codegen_masks_and_cta_sizes(oracle, spv, monkeypatch):
     """SP-table kernel: the previous round structure (mask 0) and the shipped
-    one (234: key XOR on R, uniform keys, FMA merges, prefetch), 256- and 1024-thread
+    one (490: key XOR on R, uniform keys, FMA merges, prefetch, PDL), 256- and 1024-thread
     CTAs (the size rule switches at 16384 blocks) and explicit work groups up
     to 1024, all keying options, both directions, against the oracle."""
     monkeypatch.setenv("T3DES_SP_VAR", str(spv))  # read at context creation
@@ -151,6 +151,32 @@ def test_rekey_between_async_launches(eng, oracle):
         st.synchronize()
         for keyhex, data, d, _, dst in outs:
             assert np.array_equal(host(dst), oracle.ecb(data, oracle.schedule_hex(keyhex), d)), (variant, keyhex)
+
+
+def test_chained_small_launches_with_foreign_kernels(eng, oracle):
+    """Small SP-table launches go out with programmatic dependent launch: a
+    launch may start while the previous kernel on the stream still runs and
+    waits for it before touching data.  Chains of our launches and PyTorch
+    kernels on one stream, without synchronisation, must see every producer's
+    output: copy -> encrypt -> xor -> decrypt -> encrypt, for sizes on both
+    sides of the PDL limit."""
+    ts = t3.triple_schedule(t3.parse_hex_key(KEYS[0]))
+    s = oracle.schedule_hex(KEYS[0])
+    eng.set_schedule(ts)
+    eng.set_variant(N.VARIANT_AUTO)
+    eng.set_launch(0, 0)
+    st = torch.cuda.current_stream().cuda_stream
+    for n in (1, 1000, 16384, 16385, 40000):
+        x = np.random.default_rng(n).integers(0, 256, 8 * n, dtype=np.uint8)
+        src = dev(x)
+        for _ in range(3):
+            t = src.clone()  # torch kernel
+            eng.ecb_device(0, t.data_ptr(), t.data_ptr(), t.numel(), st)
+            t.bitwise_xor_(0x5A)  # torch kernel reading our output
+            eng.ecb_device(1, t.data_ptr(), t.data_ptr(), t.numel(), st)
+            eng.ecb_device(0, t.data_ptr(), t.data_ptr(), t.numel(), st)
+        want = oracle.ecb(oracle.ecb(oracle.ecb(x, s, 0) ^ np.uint8(0x5A), s, 1), s, 0)
+        assert np.array_equal(host(t), want), n
 
 
 def test_device_errors(eng):
