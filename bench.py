@@ -4,21 +4,32 @@
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-One step = one pass of the hot path over one batch: ECB-encrypt the
-rank's 1 GiB shard (134,217,728 blocks; BASELINE configs[1], "encrypt 1 GB
-device-resident") with the bench key of the reference harness
-(bench.cpp:15-16).  Under torchrun each rank (one GPU) owns its own 1 GiB
-block range of one global stream (weak scaling, no data-path collective;
-the only collectives are the timing barrier and the max-over-ranks).
+One step = one pass of the hot path over one batch, ECB-encrypt under the
+bench key of the reference harness (bench.cpp:15-16):
+  N = 1  BASELINE configs[1]: 1 GiB (134,217,728 blocks) device-resident;
+  N > 1  BASELINE configs[3]: 64 GiB (8,589,934,592 blocks) split into N
+         contiguous block ranges (t3des_cu_shard_range), one rank per GPU,
+         each rank generating its own range of the one global payload on its
+         device (strong scaling; no data-path collective — the only
+         collectives are the timing barrier, the max over ranks and the
+         gather of the per-shard checksums, whose sum must equal the
+         reference's checksum of the whole 64 GiB ciphertext,
+         tests/golden/c3_checksum.json).
+`--gpus N` without torchrun re-launches itself under torch.distributed.run
+with N ranks; a run whose WORLD_SIZE differs from --gpus exits non-zero.
 
 value  = whole-job GB/s (decimal) from CUDA events on the launch stream,
-         inputs resident in HBM (1 GiB per step > 126 MB L2, so no flush);
+         inputs resident in HBM (>= 1 GiB per rank per step > 126 MB L2, so no
+         flush);
 e2e    = the same metric through the C ABI's host-buffer entry
-         (t3des_cu_ecb_host: pinned H2D -> kernel -> D2H inside the timing);
+         (t3des_cu_ecb_host: pinned H2D -> kernel -> D2H inside the timing),
+         next to its ceiling (pinned copy rates measured with CUDA events) and
+         the pageable-span path a reference caller's std::vector takes;
 roofline = the LOP3-issue roofline of SURVEY.md §8d: W_alg = 402 lane-ops
          per block; peak = SMs x 64 lane-ops/clk x sm_max_mhz.
 cpu_baseline = the reference's own OpenMP CPU path (oracle/_ref, Backend::
-         Threaded, all host threads) on a bounded sample, rank 0 at N=1.
+         Threaded) on the full 1 GiB, all host threads and 1 thread, rank 0 at
+         N=1.
 """
 from __future__ import annotations
 
@@ -118,70 +129,123 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(sm), "source": "nvml"}
 
 
-def cpu_reference_arm(nbytes_target_s: float = 12.0):
-    """Time the reference's own CPU implementation of the path: oracle/_ref
-    (Backend::Threaded, OpenMP, all host threads) when it was compiled, else
-    the C restatement (oracle/liboracle.so, fused route, OpenMP).  Returns
-    (GB/s, cores, kind, sample description)."""
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def golden_c3() -> dict | None:
+    """Reference checksums of the configs[3] payload/ciphertext
+    (tests/golden/c3_checksum.json, made by tests/golden/make_c3_checksum.py
+    with the reference's own encrypt_batch)."""
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "c3_checksum.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
+
+
+class CpuRef:
+    """The reference's own CPU implementation of the path: oracle/_ref
+    (encrypt_batch, Backend::Threaded, OpenMP) when it was compiled, else the
+    C restatement (oracle/liboracle.so, fused route, OpenMP) — test/baseline
+    infrastructure, only ever timed here, never the product."""
+
+    def __init__(self):
+        from tests.oracle_util import Oracle
+
+        self.o = Oracle.load()
+        self.s = self.o.schedule_hex(BENCH_KEY)
+        self.kind = "reference" if self.o.ref is not None else "port"
+
+    def threads(self, workers: int) -> int:
+        if self.o.ref is not None:
+            return int(self.o.ref.ref_resolve_workers(workers))
+        return workers or (os.cpu_count() or 1)
+
+    def payload(self, nbytes: int):
+        # the first nbytes of the bench's global payload (block i =
+        # splitmix64(seed ^ i), big-endian) — the same bytes our arm encrypts
+        return self.o.splitmix(0, nbytes // 8, SEED)
+
+    def encrypt(self, buf, out, workers: int) -> float:
+        t0 = time.perf_counter()
+        if self.o.ref is not None:
+            rc = self.o.ref.ref_ecb(buf.ctypes.data, out.ctypes.data, buf.nbytes, self.s, 0, 1, workers, 0, 0)
+        else:
+            rc = self.o.lib.oracle_ecb(buf.ctypes.data, out.ctypes.data, buf.nbytes, self.s, 0, 1, workers)
+        dt = time.perf_counter() - t0
+        assert rc == 0, rc
+        return dt
+
+    def what(self) -> str:
+        return ("reference encrypt_batch, Backend::Threaded (oracle/_ref, -O3 -DNDEBUG -fopenmp), "
+                "chunk_blocks 131072, work_group 256" if self.kind == "reference" else
+                "C restatement of the reference (oracle/liboracle.so, fused SP route, OpenMP)")
+
+
+def cpu_reference_arm(full_bytes: int = 1 << 30, one_thread_bytes: int = 64 << 20) -> dict:
+    """SURVEY §8d CPU rows: the full 1 GiB configs[1] payload on all host
+    threads (1 warm-up + min of 3, as the reference harness, bench.cpp:97-109),
+    and workers = 1 on a bounded sample (1 warm-up + min of 2)."""
     import numpy as np
 
-    from tests.oracle_util import Oracle
-
-    o = Oracle.load()
-    s = o.schedule_hex(BENCH_KEY)
-    cores = os.cpu_count() or 1
-
-    def run(buf, out):
-        if o.ref is not None:
-            rc = o.ref.ref_ecb(buf.ctypes.data, out.ctypes.data, buf.nbytes, s, 0, 1, 0, 0, 0)
-        else:
-            rc = o.lib.oracle_ecb(buf.ctypes.data, out.ctypes.data, buf.nbytes, s, 0, 1, 0)
-        assert rc == 0
-
-    kind = "reference" if o.ref is not None else "port"
-    if o.ref is not None:
-        cores = int(o.ref.ref_resolve_workers(0))
-    probe = o.payload(8 << 20)
-    out = np.empty_like(probe)
-    run(probe, out)  # warm-up
-    t0 = time.perf_counter()
-    run(probe, out)
-    rate = probe.nbytes / max(time.perf_counter() - t0, 1e-9)
-    sample = int(min(1 << 30, max(8 << 20, rate * nbytes_target_s / 2))) // 8 * 8
-    buf = o.payload(sample)
+    r = CpuRef()
+    buf = r.payload(full_bytes)
     out = np.empty_like(buf)
-    best = None
-    for _ in range(2):
-        t0 = time.perf_counter()
-        run(buf, out)
-        dt = time.perf_counter() - t0
-        best = dt if best is None else min(best, dt)
-    gbs = sample / best / 1e9
-    desc = (f"encrypt of {sample >> 20} MiB make_payload(seed 0x3DE5C0DE) with the bench key, "
-            f"{'reference encrypt_batch Backend::Threaded' if kind == 'reference' else 'oracle port'}, "
-            f"chunk 131072 / work_group 256, {cores} threads, min of 2")
-    return gbs, cores, kind, desc
+    r.encrypt(buf, out, 0)  # warm-up (threads, page faults of `out`)
+    best = min(r.encrypt(buf, out, 0) for _ in range(3))
+    cores = r.threads(0)
+    small, sout = buf[:one_thread_bytes], out[:one_thread_bytes]
+    r.encrypt(small[: 8 << 20], sout[: 8 << 20], 1)
+    best1 = min(r.encrypt(small, sout, 1) for _ in range(2))
+    return {
+        "value": round(full_bytes / best / 1e9, 4), "unit": "GB/s", "cores": cores, "kind": r.kind,
+        "sample": f"encrypt of the full {full_bytes >> 20} MiB configs[1] payload (the bench's splitmix stream, "
+                  f"bench key), {r.what()}, workers=0 -> {cores} threads, 1 warm-up + min of 3",
+        "cpu_model": cpu_model(), "host_threads": os.cpu_count(),
+        "workers_1": {"value": round(one_thread_bytes / best1 / 1e9, 4), "unit": "GB/s", "cores": 1,
+                      "sample": f"first {one_thread_bytes >> 20} MiB of the same payload, workers=1, "
+                                "1 warm-up (8 MiB) + min of 2"},
+    }
 
 
 def run_reference_impl(args, rank: int, world: int) -> None:
+    """--impl reference: the reference's CPU path on this box's host cores,
+    rank 0 only (other ranks exit without work).  Each step encrypts the
+    first 1 GiB of the workload's payload with all host threads (at N = 1 that
+    is the whole configs[1] batch; at N > 1 a 1 GiB sample of the 64 GiB
+    configs[3] stream — 64 GiB would take ~3 min per step on 16 threads)."""
     if rank != 0:
         return
-    import numpy as np  # noqa: F401
+    import numpy as np
 
-    per_step = []
-    gbs = cores = kind = desc = None
-    for i in range(args.warmup + args.steps):
-        g, cores, kind, desc = cpu_reference_arm(nbytes_target_s=4.0)
-        if i >= args.warmup:
-            per_step.append(g)
-    gbs = sorted(per_step)[len(per_step) // 2]
+    r = CpuRef()
+    nbytes = 1 << 30
+    buf = r.payload(nbytes)
+    out = np.empty_like(buf)
+    for _ in range(args.warmup):
+        r.encrypt(buf, out, 0)
+    times = [r.encrypt(buf, out, 0) for _ in range(args.steps)]
+    gbs = args.steps * nbytes / sum(times) / 1e9
+    cores = r.threads(0)
+    sample = (f"{'whole' if world == 1 else 'sample of the'} workload: encrypt of {nbytes >> 20} MiB (the first GiB "
+              f"of the bench's splitmix stream, bench key) per step, {r.what()}, workers=0 -> {cores} threads; "
+              f"value = {args.steps} steps x {nbytes >> 20} MiB / their total time (best step "
+              f"{nbytes / min(times) / 1e9:.4f} GB/s); cpu: {cpu_model()}")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(gbs, 4), "unit": "GB/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * sum(times) / args.steps, 3),
+        "higher_is_better": True, "scaling": "weak" if world == 1 else "strong",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": workload_config(args, world),
-        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": cores, "kind": kind,
-                         "sample": desc + " per step (median of steps)"},
+        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": cores, "kind": r.kind, "sample": sample},
         "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -199,24 +263,84 @@ def executed_alu_ops_per_block() -> float:
     return round(48 * (total + 32) / 32 + 4 * (64 + 96 + 48) / 32, 2)
 
 
-def pcie_bidir(host, nbytes: int) -> float:
-    """Raw pinned-host <-> device copy rate with both directions in flight
-    (the ceiling of the e2e number), GB/s each way."""
-    import torch
 
-    d_in = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
-    d_out = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
-    h2 = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+def pcie_ceiling(torch, nbytes: int = 256 << 20, iters: int = 8) -> dict:
+    """Pinned host <-> device copy rates, the ceiling of the e2e number:
+    H2D alone, D2H alone, and both directions at once on two streams (each
+    `iters` x nbytes), timed with CUDA events on the copy streams."""
+    h_in = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    h_out = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d_a = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    d_b = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
     s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(2):
-        with torch.cuda.stream(s1):
-            d_in.copy_(host, non_blocking=True)
-        with torch.cuda.stream(s2):
-            h2.copy_(d_out, non_blocking=True)
-    torch.cuda.synchronize()
-    return round(2 * nbytes / (time.perf_counter() - t0) / 1e9, 2)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def run(h2d: bool, d2h: bool) -> float:
+        torch.cuda.synchronize()
+        start, e1, e2 = ev(), ev(), ev()
+        start.record(s1)
+        s2.wait_event(start)
+        for _ in range(iters):
+            if h2d:
+                with torch.cuda.stream(s1):
+                    d_a.copy_(h_in, non_blocking=True)
+            if d2h:
+                with torch.cuda.stream(s2):
+                    h_out.copy_(d_b, non_blocking=True)
+        e1.record(s1)
+        e2.record(s2)
+        torch.cuda.synchronize()
+        ms = max(start.elapsed_time(e1) if h2d else 0.0, start.elapsed_time(e2) if d2h else 0.0)
+        return iters * nbytes / (ms * 1e-3) / 1e9
+
+    run(True, True)  # warm-up
+    out = {"h2d_gbs": round(run(True, False), 2), "d2h_gbs": round(run(False, True), 2),
+           "bidir_gbs_each_way": round(run(True, True), 2),
+           "how": f"{iters} x {nbytes >> 20} MiB pinned copies per direction, CUDA events on the copy streams"}
+    del h_in, h_out, d_a, d_b
+    return out
+
+
+def self_launch(args) -> int | None:
+    """--gpus N > 1 outside torchrun: re-run this script under
+    torch.distributed.run with N ranks (one per GPU) on 127.0.0.1."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import socket
+    import subprocess
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def bind_to_gpu_cpus(device: int) -> dict:
+    """Pin this rank's threads to the CPUs NVML reports as local to its GPU
+    (the GPU's NUMA node), so its pinned staging, copy threads and PCIe
+    traffic stay on one socket.  Returns what was done."""
+    try:
+        import pynvml
+        import torch
+
+        pynvml.nvmlInit()
+        uuid = str(torch.cuda.get_device_properties(device).uuid)
+        h = pynvml.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        cpus = {64 * w + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1}
+        cpus &= os.sched_getaffinity(0)
+        if not cpus or cpus == os.sched_getaffinity(0):
+            return {"bound": False, "cpus": len(os.sched_getaffinity(0)), "why": "GPU is local to every allowed CPU"}
+        os.sched_setaffinity(0, cpus)
+        return {"bound": True, "cpus": len(cpus)}
+    except Exception as exc:  # NVML absent or no affinity info
+        return {"bound": False, "why": type(exc).__name__}
+
+
+def u64_to_i64(x: int) -> int:
+    return x - (1 << 64) if x >= (1 << 63) else x
 
 
 def nist_kat_ok(t3) -> bool:
@@ -244,6 +368,7 @@ def cross_check(e, N, torch, src, dst, nblocks, stream, variant) -> bool:
     e.ecb_device(1, dst.data_ptr(), dst.data_ptr(), 8 * nblocks, stream)
     ok = bool(torch.equal(got, ref)) and e.checksum(dst.data_ptr(), 0, nblocks, stream) == cs_in
     return ok
+
 
 
 def extra_configs(e, t3, N, torch, np) -> dict:
@@ -350,37 +475,63 @@ def extra_configs(e, t3, N, torch, np) -> dict:
     del b1, b2
     e3.close()
     torch.cuda.empty_cache()
-    # configs[3]: 64 GiB in block-range shards; on one device the G shards
-    # run back to back (the torchrun bench runs them on G GPUs)
+    # configs[3]: the 64 GiB stream on one device — one launch, and the 8
+    # block ranges 8 GPUs would own run back to back — checked against the
+    # reference's checksum of the whole 64 GiB ciphertext
     from paper_1305_4376_b200.sharding import shard_range
 
     n64 = (64 << 30) // 8
     free, _ = torch.cuda.mem_get_info()
+    gold = golden_c3()
     if free >= 8 * n64 + (4 << 30):
         big = torch.empty(8 * n64, dtype=torch.uint8, device="cuda")
         e.fill_splitmix(big.data_ptr(), 0, n64, SEED, stream)
-        sums, times = {}, {}
-        e.ecb_device(1, big.data_ptr(), big.data_ptr(), 8 * n64, stream)  # warm-up pair
-        e.ecb_device(0, big.data_ptr(), big.data_ptr(), 8 * n64, stream)
-        for g in (1, 8):  # each g: decrypt the payload P in g shard ranges, checksum, restore P
+        e.ecb_device(0, big.data_ptr(), big.data_ptr(), 8 * n64, stream)  # warm-up pair
+        e.ecb_device(1, big.data_ptr(), big.data_ptr(), 8 * n64, stream)
+        sums, times, plain_ok = {}, {}, True
+        for g in (1, 8):  # each g: encrypt the payload in place as g shard ranges, checksum, decrypt back
             torch.cuda.synchronize()
             ev0.record()
             for r in range(g):
                 first, count = shard_range(n64, g, r)
-                e.ecb_device(1, big.data_ptr() + 8 * first, big.data_ptr() + 8 * first, 8 * count, stream)
+                e.ecb_device(0, big.data_ptr() + 8 * first, big.data_ptr() + 8 * first, 8 * count, stream)
             ev1.record()
             torch.cuda.synchronize()
             times[g] = ev0.elapsed_time(ev1)
             sums[g] = e.checksum(big.data_ptr(), 0, n64, stream)
-            e.ecb_device(0, big.data_ptr(), big.data_ptr(), 8 * n64, stream)
+            e.ecb_device(1, big.data_ptr(), big.data_ptr(), 8 * n64, stream)
+            if gold:
+                plain_ok = plain_ok and e.checksum(big.data_ptr(), 0, n64, stream) == int(gold["plaintext_checksum"], 16)
+        want = int(gold["ciphertext_checksum"], 16) if gold else None
         out["c3_64GiB_block_range_shards"] = {
-            "device_GBps_1_shard": round(8 * n64 / times[1] / 1e6, 2),
+            "device_GBps_1_launch": round(8 * n64 / times[1] / 1e6, 2),
             "device_GBps_8_shards_back_to_back": round(8 * n64 / times[8] / 1e6, 2),
+            "ciphertext_checksum": f"{sums[1]:016x}",
             "checksum_equal_1_vs_8_shards": sums[1] == sums[8],
-            "note": "in-place decrypt of 64 GiB on one B200; the 8 shard ranges are the ones 8 GPUs would own"}
+            "checksum_equal_to_reference": (sums[1] == want and sums[8] == want and plain_ok) if gold else None,
+            "note": "in-place encrypt of 64 GiB on one B200; the 8 shard ranges are the ones 8 GPUs own; "
+                    "reference checksum from tests/golden/c3_checksum.json (reference encrypt_batch)"}
         del big
         torch.cuda.empty_cache()
     return out
+
+
+def workload_config(args, world: int) -> dict:
+    if world == 1:
+        wl = (f"BASELINE configs[1]: 3DES-ECB encrypt {args.gib} GiB device-resident on 1 B200 "
+              f"(configs[3], 64 GiB in block ranges, is the N>1 workload and a configs_measured leg here)")
+        n = (args.gib << 30) // 8
+    else:
+        wl = (f"BASELINE configs[3]: 3DES-ECB encrypt {args.c3_gib} GiB device-resident, split into {world} "
+              f"contiguous block ranges (t3des_cu_shard_range), one per GPU")
+        n = (args.c3_gib << 30) // 8
+    return {
+        "workload": wl, "key": BENCH_KEY, "keying_option": 1,
+        "global_blocks": n, "blocks_per_gpu": n // world,
+        "variant": args.variant, "payload": "block i = splitmix64(0x3DE5C0DE ^ i), big-endian, generated on device",
+        "l2_policy": "inputs larger than L2 (>= 1 GiB per rank per step vs 126 MB L2), no flush",
+        "parallelism": f"block-range shards x{world}, no data-path collective",
+    }
 
 
 def _splitmix_checksum(e, torch, n) -> int:
@@ -391,16 +542,6 @@ def _splitmix_checksum(e, torch, n) -> int:
     return v
 
 
-def workload_config(args, world: int) -> dict:
-    return {
-        "workload": f"3DES-ECB encrypt {args.gib} GiB device-resident per GPU (BASELINE configs[1]); "
-                    f"N>1: block-range shards of one stream (configs[3])",
-        "key": BENCH_KEY, "keying_option": 1,
-        "blocks_per_gpu": (args.gib << 30) // 8, "global_blocks": world * ((args.gib << 30) // 8),
-        "variant": args.variant, "payload": "splitmix64(seed ^ block index) generated on device",
-        "l2_policy": "inputs larger than L2 (1 GiB per step vs 126 MB L2), no flush",
-        "parallelism": f"block-range shards x{world}, no data-path collective",
-    }
 
 
 def main() -> None:
@@ -410,7 +551,8 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--variant", choices=["bitslice", "bitslice_alu", "bitslice_dfma", "bitslice_shrfma", "bitslice_ldg", "sptable"], default="bitslice")
-    ap.add_argument("--gib", type=int, default=1, help="GiB per GPU per step")
+    ap.add_argument("--gib", type=int, default=1, help="GiB per step at N = 1 (configs[1])")
+    ap.add_argument("--c3-gib", type=int, default=64, help="global GiB per step at N > 1 (configs[3])")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
@@ -420,7 +562,13 @@ def main() -> None:
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
+    rc = self_launch(args)
+    if rc is not None:
+        sys.exit(rc)
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference_impl(args, rank, world)
         return
@@ -435,8 +583,14 @@ def main() -> None:
     # logic run with several ranks on one GPU (ranks never wait on each
     # other's kernels; NCCL refuses two ranks on one device)
     backend = os.environ.get("T3DES_BENCH_DIST_BACKEND", "nccl")
-    device = local % max(torch.cuda.device_count(), 1)
+    ndev = torch.cuda.device_count()
+    if backend == "nccl" and world > ndev:
+        print(f"bench.py: {world} ranks need {world} GPUs, {ndev} visible "
+              f"(T3DES_BENCH_DIST_BACKEND=gloo shares one GPU between ranks)", file=sys.stderr)
+        sys.exit(2)
+    device = local % max(ndev, 1)
     torch.cuda.set_device(device)
+    numa = bind_to_gpu_cpus(device) if world > 1 else {"bound": False, "why": "N = 1"}
     if world > 1:
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", device))
@@ -456,6 +610,15 @@ def main() -> None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def gather_ints(x: int) -> list[int]:
+        if world == 1:
+            return [x]
+        dev_ = "cuda" if backend == "nccl" else "cpu"
+        t = torch.tensor([x], dtype=torch.int64, device=dev_)
+        parts = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(parts, t)
+        return [int(p.item()) for p in parts]
+
     e = t3.Engine(device)
     ts = t3.triple_schedule(t3.parse_hex_key(BENCH_KEY))
     e.set_schedule(ts)
@@ -465,8 +628,8 @@ def main() -> None:
     e.set_variant(VARIANTS[args.variant])
     from paper_1305_4376_b200.sharding import shard_range
 
-    per_rank = (args.gib << 30) // 8
-    first_block, nblocks = shard_range(world * per_rank, world, rank)  # == rank * per_rank
+    n_global = ((args.gib if world == 1 else args.c3_gib) << 30) // 8
+    first_block, nblocks = shard_range(n_global, world, rank)
     nbytes = 8 * nblocks
     stream = torch.cuda.Stream()
     sp = stream.cuda_stream
@@ -496,12 +659,30 @@ def main() -> None:
             e.ecb_device(0, src.data_ptr(), dst.data_ptr(), nbytes, sp)
         ev1.record(stream)
         barrier()
-    launches = e.launch_count() - l0
+    launches = sum(gather_ints(e.launch_count() - l0))
     ms_total = ev0.elapsed_time(ev1)
     ms_step = max_over_ranks(ms_total / args.steps)
-    gbs = world * nbytes / (ms_step * 1e-3) / 1e9
-    blocks_per_s = world * nblocks / (ms_step * 1e-3)
+    gbs = 8 * n_global / (ms_step * 1e-3) / 1e9
     clocks = clk.summary()
+
+    # the output of the timed steps against the reference's checksums: the
+    # per-shard checksums add up to the reference checksum of the whole
+    # stream (tests/golden/c3_checksum.json; its 1 GiB pieces cover configs[1])
+    gold = golden_c3()
+    shard_sums = gather_ints(u64_to_i64(e.checksum(dst.data_ptr(), first_block, nblocks, sp)))
+    total_sum = sum(shard_sums) % 2**64
+    want = None
+    if gold and world > 1 and args.c3_gib == 64:
+        want = int(gold["ciphertext_checksum"], 16)
+    elif gold and world == 1 and args.gib == 1:
+        want = int(gold["piece_ciphertext_checksums"][0], 16)
+    output_check = {"checksum": f"{total_sum:016x}", "reference_checksum": f"{want:016x}" if want is not None else None,
+                    "checksum_equal_to_reference": (total_sum == want) if want is not None else None}
+    if world > 1:
+        output_check["checksum_equal_to_N1"] = output_check["checksum_equal_to_reference"]
+        output_check["how"] = ("sum of the ranks' shard checksums == the single-run checksum of the 64 GiB "
+                               "ciphertext (reference encrypt_batch, tests/golden/c3_checksum.json; the N=1 "
+                               "configs[3] leg reproduces it on one GPU)")
 
     peaks = measured_peaks()
     sms = torch.cuda.get_device_properties(device).multi_processor_count
@@ -522,6 +703,7 @@ def main() -> None:
         "bound": "alu", "achieved": round(achieved, 4), "peak": round(peak_tlops, 4), "unit": "Tlop3/s",
         "frac": round(achieved / peak_tlops, 4), "traffic": traffic,
         "kernel_ms": round(ms_step, 4),
+        "per": "one GPU (rank 0's shard at N > 1; the slowest rank sets ms_per_step)",
         "peak_source": f"{sms} SMs x {ALU_LANES_PER_CLK_PER_SM} ALU lanes/clk (LOP3 issue rate measured by "
                        f"tools/microbench/pipe_rates.cu, profiles/r1/pipe_rates_b200.txt) x sm_max_mhz {fmax:.0f} "
                        f"({'MEASURED_PEAKS.json' if 'sm_max_mhz' in peaks else 'fallback'})",
@@ -529,8 +711,9 @@ def main() -> None:
                               if clocks.get("sm_mhz") else None),
         "w_alg_lane_ops_per_block": W_ALG,
         # what the shipped kernel actually issues to the ALU pipe per block
-        # (static SASS-level count: S-box LOP3 + Feistel LOP3 per round, plus
-        # the slice transposes), and the utilisation that implies
+        # (static count: S-box LOP3 + Feistel LOP3 per round, plus the slice
+        # transposes; tests/test_sass.py pins it to the binary), and the
+        # utilisation that implies
         "executed_alu_lane_ops_per_block": alu_ops,
         "alu_pipe_frac": round(per_gpu_bps * alu_ops / (peak_tlops * 1e12), 4),
         "hbm": {"achieved_gbs": round(per_gpu_bps * 16 / 1e9, 2), "peak_gbs": hbm_peak,
@@ -539,16 +722,21 @@ def main() -> None:
 
     line = {
         "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+        "scaling": "weak" if world == 1 else "strong",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": workload_config(args, world),
         "roofline": roofline, "clocks": clocks, "gpu_launches": int(launches),
         "self_check": {"ok": parity_ok, "how": "NIST SP 800-67 KAT via the engine; bitsliced == SP-table kernel "
                        "on a 1/4096 sample; decrypt(encrypt(x)) == x checksum"},
+        "output_check": output_check,
     }
+    if world > 1:
+        line["numa"] = numa
+        line["dist_backend"] = backend
 
     # the other variants (north star: bitsliced vs SP-table, ncu picks)
-    if not args.no_variants:
+    if not args.no_variants and world == 1:
         line["variants"] = {args.variant: round(gbs, 3)}
         for other, code in VARIANTS.items():
             if other == args.variant:
@@ -567,49 +755,101 @@ def main() -> None:
             line["variants"][other] = round(world * nbytes / (ms2 * 1e-3) / 1e9, 3)
         e.set_variant(VARIANTS[args.variant])
 
+    # N > 1: the weak-scaling figure next to it — 1 GiB per rank (the first
+    # GiB of each rank's range), checked against the reference's per-GiB
+    # checksums
+    one = min(nbytes, 1 << 30)
+    if world > 1:
+        for _ in range(2):
+            e.ecb_device(0, src.data_ptr(), dst.data_ptr(), one, sp)
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            e.ecb_device(0, src.data_ptr(), dst.data_ptr(), one, sp)
+        ev1.record(stream)
+        barrier()
+        msw = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+        cs = e.checksum(dst.data_ptr(), first_block, one // 8, sp)
+        ok = None
+        if gold and args.c3_gib == 64 and one == 1 << 30 and first_block % (1 << 27) == 0:
+            ok = cs == int(gold["piece_ciphertext_checksums"][first_block >> 27], 16)
+        oks = gather_ints(-1 if ok is None else int(ok))
+        line["weak_1GiB_per_gpu"] = {
+            "value": round(world * one / (msw * 1e-3) / 1e9, 3), "unit": "GB/s", "ms_per_step": round(msw, 4),
+            "steps": args.steps, "checksums_equal_to_reference": None if -1 in oks else all(oks),
+            "how": "each rank encrypts the first GiB of its own block range; max over ranks"}
+
     del dst
     torch.cuda.empty_cache()
 
-    # end to end through the C ABI host entry (pinned H2D + kernel + D2H)
+    # end to end through the C ABI host entry (pinned H2D + kernel + D2H);
+    # 1 GiB per rank (host RAM bounds it at N > 1; weak)
     if not args.no_e2e:
-        host = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
-        host.copy_(src.cpu())
+        host = torch.empty(one, dtype=torch.uint8).pin_memory()
+        host.copy_(src[:one].cpu())
         del src
         torch.cuda.empty_cache()
-        e.ecb_host(0, host.data_ptr(), host.data_ptr(), nbytes)  # warm (allocates staging)
-        k3 = max(3, min(args.steps, 5))
+        e.ecb_host(0, host.data_ptr(), host.data_ptr(), one)  # warm (allocates staging)
+        k3 = max(5, min(args.steps, 8))
         barrier()
         t0 = time.perf_counter()
         for _ in range(k3):
-            e.ecb_host(0, host.data_ptr(), host.data_ptr(), nbytes)
+            e.ecb_host(0, host.data_ptr(), host.data_ptr(), one)
         dt = max_over_ranks((time.perf_counter() - t0) / k3)
-        line["e2e"] = {"value": round(world * nbytes / dt / 1e9, 3), "unit": "GB/s",
-                       "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
-                       "path": "t3des_cu_ecb_host, pinned host buffer, default pipeline (3 streams, 32 MiB stages for 1 GiB)",
-                       "steps": k3, "pcie_bidir_copy_gbs_each_way": pcie_bidir(host, nbytes)}
+        line["e2e"] = {"value": round(world * one / dt / 1e9, 3), "unit": "GB/s",
+                       "h2d_bytes_per_step": world * one, "d2h_bytes_per_step": world * one,
+                       "path": f"t3des_cu_ecb_host, pinned host buffer, {one >> 20} MiB per rank, in place, "
+                               "default pipeline (3 streams, 32 MiB stages with an 8 MiB ramp)",
+                       "steps": k3, "timing": "host wall clock around the synchronous C-ABI call, max over ranks"}
+        # the ceiling: pinned copy rates measured with CUDA events
+        ceil = pcie_ceiling(torch)
+        line["e2e"]["pcie"] = ceil
+        line["e2e"]["frac_of_bidir_ceiling"] = round((one / dt / 1e9) / ceil["bidir_gbs_each_way"], 3)
         # the same call from pageable memory (what a reference caller's
         # std::vector is): staged through the engine's pinned ring by host
         # copy threads
         page = host.numpy().copy()
-        e.ecb_host(0, page.ctypes.data, page.ctypes.data, nbytes)
+        e.ecb_host(0, page.ctypes.data, page.ctypes.data, one)
         barrier()
         t0 = time.perf_counter()
         for _ in range(k3):
-            e.ecb_host(0, page.ctypes.data, page.ctypes.data, nbytes)
+            e.ecb_host(0, page.ctypes.data, page.ctypes.data, one)
         dtp = max_over_ranks((time.perf_counter() - t0) / k3)
-        line["e2e"]["pageable"] = {"value": round(world * nbytes / dtp / 1e9, 3), "unit": "GB/s",
+        line["e2e"]["pageable"] = {"value": round(world * one / dtp / 1e9, 3), "unit": "GB/s",
                                    "path": "t3des_cu_ecb_host, pageable host buffer (numpy), in place"}
         del page
+        # one process driving all N GPUs through t3des_cu_ecb_multi (the
+        # workers axis of DispatchConfig): rank 0, the other ranks idle
+        barrier()
+        if rank == 0:
+            devs = [r % max(ndev, 1) for r in range(world)]
+            mh = torch.empty(world * one, dtype=torch.uint8).pin_memory()
+            for r in range(world):
+                mh[r * one:(r + 1) * one].copy_(host)
+            cdevs = (ctypes.c_int * world)(*devs)
+            sub = ts.sub48()
+            f = N.lib().t3des_cu_ecb_multi
+            rc = f(cdevs, world, sub, 0, mh.data_ptr(), mh.data_ptr(), mh.numel())
+            t0 = time.perf_counter()
+            for _ in range(k3):
+                rc = rc or f(cdevs, world, sub, 0, mh.data_ptr(), mh.data_ptr(), mh.numel())
+            dtm = (time.perf_counter() - t0) / k3
+            line["e2e"]["multi"] = {"value": round(world * one / dtm / 1e9, 3) if rc == 0 else None, "unit": "GB/s",
+                                    "devices": devs, "bytes": world * one, "status": N.strerror(rc),
+                                    "path": "t3des_cu_ecb_multi from one process (one host thread + context per "
+                                            "device, pinned buffer), the GPU reading of DispatchConfig.workers"}
+            del mh
+        barrier()
         del host
     else:
         line["e2e"] = None
+        del src
 
     if not args.no_extra_configs and world == 1:
         line["configs_measured"] = extra_configs(e, t3, N, torch, np)
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        g, cores, kind, desc = cpu_reference_arm()
-        line["cpu_baseline"] = {"value": round(g, 4), "unit": "GB/s", "cores": cores, "kind": kind, "sample": desc}
+        line["cpu_baseline"] = cpu_reference_arm()
 
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -129,17 +129,32 @@ int t3des_cu_ecb_host(t3des_cu_ctx* ctx, int direction, const uint8_t* in, uint8
 int t3des_cu_set_pipeline(t3des_cu_ctx* ctx, size_t chunk_bytes, int streams);
 
 /* Host buffers sharded by contiguous block ranges (multiples of 1024
- * blocks) over `ndev` devices, one host thread and context per device; no
- * collective.  Blocks are independent, so the result equals
- * the single-device result. */
+ * blocks) over `ndev` devices, one host thread and (pooled) context per
+ * device; no collective.  Blocks are independent, so the result
+ * equals the single-device result.  Where the host has several NUMA nodes,
+ * each shard's submitting thread, host copy threads and pinned staging ring
+ * are placed on its GPU's node (sysfs; T3DES_NUMA=0 disables). */
 int t3des_cu_ecb_multi(const int* devices, int ndev, const uint64_t sub48[48], int direction,
                        const uint8_t* in, uint8_t* out, size_t len);
+
+/* The GPU reading of the reference's DispatchConfig.workers
+ * (dispatch.hpp:28, the worker count its run_chunk hands to OpenMP,
+ * dispatch.cpp:73-84): `workers` shards (0 = 1) of the host batch, assigned
+ * round-robin to the visible devices starting at first_device — workers = 8
+ * on an 8-GPU node uses every GPU once, workers = 2 on one GPU runs two
+ * contexts on it.  workers <= 1 runs on a pooled context of first_device;
+ * otherwise t3des_cu_ecb_multi over that device list.  Synchronous.  This is
+ * what the patched reference's Backend::Cuda calls. */
+int t3des_cu_ecb_workers(unsigned workers, int first_device, const uint64_t sub48[48], int direction,
+                         const uint8_t* in, uint8_t* out, size_t len);
 
 /* Device-resident multi-GPU (NVLink 5 / NVSwitch): din/dout
  * live on `home_device`; shard g (t3des_cu_shard_range) is copied to
  * devices[g] with cudaMemcpyPeerAsync, transformed there and copied back.
  * A shard whose device is the home device is transformed in place of
  * din -> dout without copies unless flags & T3DES_CU_MULTI_STAGE_ALL.
+ * Each staged shard is pipelined in chunks over three streams of its device
+ * (peer copy in, kernel, peer copy out overlap chunk by chunk).
  * Synchronous.  Peer access is enabled where the topology allows it. */
 #define T3DES_CU_MULTI_STAGE_ALL 1
 int t3des_cu_ecb_multi_device(const int* devices, int ndev, const uint64_t sub48[48], int direction,

@@ -29,6 +29,23 @@ int main() {
         decrypt_batch(gpu, back, ts, c_gpu);
         if (back != in) { std::printf("decrypt mismatch n=%zu\n", n); return 1; }
     }
+    // cfg.workers > 1: that many block-range shards round-robin over the
+    // visible GPUs (workers = 2 on a one-GPU box: two contexts on it)
+    for (unsigned w : {2u, 3u}) {
+        for (std::size_t n : {1ul, 2047ul, 100003ul, 3ul << 20}) {
+            std::vector<std::uint8_t> in(8 * n), cpu(in.size()), gpu(in.size()), back(in.size());
+            for (auto& b : in) b = static_cast<std::uint8_t>(rng());
+            DispatchConfig c_cpu, c_gpu;
+            c_cpu.backend = Backend::Threaded;
+            c_gpu.backend = Backend::Cuda;
+            c_gpu.workers = w;
+            encrypt_batch(in, cpu, ts, c_cpu);
+            encrypt_batch(in, gpu, ts, c_gpu);
+            if (gpu != cpu) { std::printf("workers=%u encrypt mismatch n=%zu\n", w, n); return 1; }
+            decrypt_batch(gpu, back, ts, c_gpu);
+            if (back != in) { std::printf("workers=%u decrypt mismatch n=%zu\n", w, n); return 1; }
+        }
+    }
     // the reference's own stream loop, chunk by chunk on the GPU backend
     std::string payload(100003, '\0');
     for (auto& ch : payload) ch = static_cast<char>(rng());

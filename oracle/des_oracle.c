@@ -294,10 +294,14 @@ static uint64_t mt64_next(mt64_t* s) {
 void oracle_make_payload(uint8_t* out, size_t bytes, uint64_t seed) {
     mt64_t s;
     mt64_seed(&s, seed);
-    uint64_t w = 0;
-    for (size_t i = 0; i < bytes; i++) {
-        if (i % 8 == 0) w = mt64_next(&s);
-        out[i] = (uint8_t)(w >> (8 * (i % 8)));
+    size_t i = 0;
+    for (; i + 8 <= bytes; i += 8) { /* one draw per 8 bytes, little-endian */
+        uint64_t w = mt64_next(&s);
+        for (int b = 0; b < 8; b++) out[i + b] = (uint8_t)(w >> (8 * b));
+    }
+    if (i < bytes) {
+        uint64_t w = mt64_next(&s);
+        for (int b = 0; i < bytes; i++, b++) out[i] = (uint8_t)(w >> (8 * b));
     }
 }
 
@@ -311,7 +315,29 @@ uint64_t oracle_splitmix_block(uint64_t seed, uint64_t i) {
 }
 
 void oracle_splitmix_payload(uint8_t* out, uint64_t first_block, size_t nblocks, uint64_t seed) {
-    for (size_t i = 0; i < nblocks; i++) store_be(oracle_splitmix_block(seed, first_block + i), out + 8 * i);
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static, 65536)
+#endif
+    for (long long i = 0; i < (long long)nblocks; i++)
+        store_be(oracle_splitmix_block(seed, first_block + (uint64_t)i), out + 8 * i);
+}
+
+/* Host restatement of the engine's shard-additive checksum
+ * (t3_checksum_kernel): sum_i splitmix(le64(block i) ^ (first_block + i)),
+ * salt 0x3DE5C0DE, mod 2^64.  Lets the full-size parity tests and the
+ * 64 GiB golden checksum (tests/golden/make_c3_checksum.py) compare whole
+ * outputs without holding two copies. */
+uint64_t oracle_checksum(const uint8_t* data, uint64_t first_block, size_t nblocks) {
+    uint64_t acc = 0;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static, 65536) reduction(+ : acc)
+#endif
+    for (long long i = 0; i < (long long)nblocks; i++) {
+        uint64_t w;
+        memcpy(&w, data + 8 * i, 8); /* little-endian load, as the kernel's */
+        acc += oracle_splitmix_block(0x3DE5C0DEull, w ^ (first_block + (uint64_t)i));
+    }
+    return acc;
 }
 
 /* ---- helpers exposed for tests ------------------------------------------ */

@@ -159,7 +159,7 @@ class Backend(enum.Enum):
 class DispatchConfig:
     chunk_blocks: int = 131072  # blocks per launch, applied only if gpu_chunked
     work_group: int = 256       # threads per CTA, applied only if gpu_chunked
-    workers: int = 0            # CUDA: number of GPUs (0 = one, `device`)
+    workers: int = 0            # CUDA: block-range shards, round-robin over the GPUs from `device` (0 = one)
     backend: Backend = Backend.CUDA
     device: int = 0
     variant: int = N.VARIANT_AUTO
@@ -304,6 +304,8 @@ def _run_batch(src, dst, ts: TripleSchedule, cfg: DispatchConfig, direction: int
             raise InputLengthError("output buffer size mismatch")
         if not (src.is_contiguous() and dst.is_contiguous()):
             raise ValueError("tensors must be contiguous")
+        if src.device != dst.device:
+            raise ValueError(f"in and out must be on the same device ({src.device} vs {dst.device})")
         if cfg.backend is Backend.NoOpCopy:
             if src.data_ptr() != dst.data_ptr():
                 dst.view(torch.uint8).copy_(src.view(torch.uint8).reshape(-1).view_as(dst.view(torch.uint8)))
@@ -328,8 +330,9 @@ def _run_batch(src, dst, ts: TripleSchedule, cfg: DispatchConfig, direction: int
     if nin == 0:
         return
     if cfg.workers and cfg.workers > 1:
-        devs = (ctypes.c_int * cfg.workers)(*range(cfg.device, cfg.device + cfg.workers))
-        _raise(N.lib().t3des_cu_ecb_multi(devs, cfg.workers, ts.sub48(), direction, pin, pout, nin))
+        # workers shards round-robin over the visible GPUs from cfg.device
+        # (t3des_cu_ecb_workers; two on one GPU = two contexts on it)
+        _raise(N.lib().t3des_cu_ecb_workers(cfg.workers, cfg.device, ts.sub48(), direction, pin, pout, nin))
         return
     e = engine(cfg.device)
     e.set_schedule(ts)

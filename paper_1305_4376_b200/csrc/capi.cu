@@ -28,24 +28,14 @@ constexpr std::uint64_t kSpMinThreads = 128;  // SP-table CTA size floor for sma
 constexpr std::size_t kZeroCopyMaxBytes = std::size_t(64) << 20;  // scripts/zerocopy_{sweep,big}.py
 // pageable batches up to this size run their stages zero-copy on the pinned slots
 constexpr std::size_t kStagedZeroCopyMaxBytes = std::size_t(12) << 20;
-// first/last stage size of the pinned DMA pipeline's ramp (large batches)
 // SP-table launches that may use PDL (scripts/pdl_ab.py: 8-128 KiB enc+dec
 // chains 12.3 -> 7.7 us per pair; from 256 KiB the early CTAs cost more)
 constexpr std::uint64_t kPdlMaxBlocks = 16384;
+// first/last stage size of the pinned DMA pipeline's ramp (large batches)
 constexpr std::size_t kRampBytes = std::size_t(8) << 20;  // scripts/ramp_sweep.py
 constexpr int kSpSmemBytes = 8 * 64 * 32 * 4 + int(sizeof(T3SpKeyParam)) + 8 * 64 * 4;  // 64 KiB tables, round keys, staging
 
-// Restores the caller's current device on scope exit.
-struct DeviceScope {
-    int prev = -1;
-    explicit DeviceScope(int dev) {
-        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
-        cudaSetDevice(dev);
-    }
-    ~DeviceScope() {
-        if (prev >= 0) cudaSetDevice(prev);
-    }
-};
+using t3b::DeviceScope;
 
 #define T3_CK(call)                                   \
     do {                                              \
@@ -349,16 +339,28 @@ int ecb_host_staged(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8
     if (const char* e = std::getenv("T3DES_HOST_STAGE_MIB")) S = std::size_t(std::max(1, std::atoi(e))) << 20;
     S = std::min(S, len);
     if (S > 8 * T3_TILE_BLOCKS) S -= S % (8 * T3_TILE_BLOCKS);
+    const t3b::NumaNode none;
+    const t3b::NumaNode& node = c->numa_bind ? c->numa : none;
     if (c->hbuf_bytes < S) {
         for (int i = 0; i < R; ++i) {
             if (c->hev_live[i]) T3_CK(cudaEventSynchronize(c->hev[i]));
-            if (c->hbuf[i]) cudaFreeHost(c->hbuf[i]);
+            t3b::host_free_on_node(c->hbuf[i], c->hbuf_bytes, c->hbuf_registered[i]);
             if (c->hdev[i]) cudaFree(c->hdev[i]);
             c->hbuf[i] = c->hdev[i] = nullptr;
         }
         c->hbuf_bytes = 0;
         for (int i = 0; i < R; ++i) {
-            T3_CK(cudaMallocHost(&c->hbuf[i], S));
+            void* hp = nullptr;
+            if (t3b::host_alloc_on_node(S, node, &hp, &c->hbuf_registered[i]) != 0) {
+                for (int j = 0; j < i; ++j) {  // keep the ring all-or-nothing
+                    t3b::host_free_on_node(c->hbuf[j], S, c->hbuf_registered[j]);
+                    if (c->hdev[j]) cudaFree(c->hdev[j]);
+                    c->hbuf[j] = c->hdev[j] = nullptr;
+                }
+                (void)cudaGetLastError();
+                return T3DES_CU_ERR_CUDA;
+            }
+            c->hbuf[i] = static_cast<std::uint8_t*>(hp);
             T3_CK(cudaMalloc(&c->hdev[i], S));
             if (!c->hev[i]) T3_CK(cudaEventCreateWithFlags(&c->hev[i], cudaEventDisableTiming));
             c->hev_live[i] = false;
@@ -372,8 +374,8 @@ int ecb_host_staged(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8
         // threads with 4 MiB stages are best (26 GB/s end to end vs 7 GB/s
         // through the driver's own pageable copies)
         if (total <= 0) total = std::clamp(int(std::thread::hardware_concurrency()) * 3 / 4, 2, 12);
-        c->pool_in = new t3b::CopyPool((total + 1) / 2);
-        c->pool_out = new t3b::CopyPool(std::max(1, total / 2));
+        c->pool_in = new t3b::CopyPool((total + 1) / 2, node);
+        c->pool_out = new t3b::CopyPool(std::max(1, total / 2), node);
     }
     const std::size_t nst = (len + S - 1) / S;
     // One small stage between two pageable spans: copy in, run the SP-table
@@ -511,12 +513,20 @@ int t3des_cu_create(int device, t3des_cu_ctx** out) {
     }
     cudaDeviceProp prop;
     T3_CK(cudaGetDeviceProperties(&prop, device));
-    if (prop.major != 10) return T3DES_CU_ERR_NO_DEVICE;  // built for sm_100a only
+    // built for sm_100a only: another 10.x part would fail every launch later
+    if (prop.major != 10 || prop.minor != 0) return T3DES_CU_ERR_NO_DEVICE;
     DeviceScope scope(device);
     auto* c = new (std::nothrow) t3des_cu_ctx();
     if (!c) return T3DES_CU_ERR_ARG;
     c->device = device;
     c->sms = prop.multiProcessorCount;
+    {
+        char bus[32] = {};
+        if (cudaDeviceGetPCIBusId(bus, sizeof bus, device) == cudaSuccess) c->numa = t3b::numa_node_of_pci(bus);
+        (void)cudaGetLastError();
+        // T3DES_NUMA=1: place single-device contexts too (multi-GPU contexts always are)
+        if (const char* e = std::getenv("T3DES_NUMA")) c->numa_bind = std::atoi(e) == 1;
+    }
     int rc = T3DES_CU_OK;
     do {
         int occ_ldg = 1;
@@ -596,7 +606,7 @@ int t3des_cu_destroy(t3des_cu_ctx* c) {
         if (c->ubuf) cudaFree(c->ubuf);
         if (c->d_spk) cudaFree(c->d_spk);
         for (int i = 0; i < t3des_cu_ctx::kHostSlots; ++i) {
-            if (c->hbuf[i]) cudaFreeHost(c->hbuf[i]);
+            t3b::host_free_on_node(c->hbuf[i], c->hbuf_bytes, c->hbuf_registered[i]);
             if (c->hdev[i]) cudaFree(c->hdev[i]);
             if (c->hev[i]) cudaEventDestroy(c->hev[i]);
         }
@@ -686,14 +696,18 @@ int t3des_cu_ecb_device(t3des_cu_ctx* c, int dir, const void* din, void* dout, s
     // caller's stream; synchronous, so the buffer is free on return.
     constexpr std::size_t kChunk = std::size_t(16) << 20;
     if (!c->ubuf) T3_CK(cudaMalloc(&c->ubuf, kChunk));
-    for (std::size_t off = 0; off < len; off += kChunk) {
+    // errors still wait for the queued copies: none may write `out` after return
+    int rc2 = T3DES_CU_OK;
+    for (std::size_t off = 0; off < len && !rc2; off += kChunk) {
         const std::size_t n = std::min(kChunk, len - off);
-        T3_CK(cudaMemcpyAsync(c->ubuf, in + off, n, cudaMemcpyDeviceToDevice, s));
-        if (int rc2 = run_device(c, dir, c->ubuf, c->ubuf, n / 8, s)) return rc2;
-        T3_CK(cudaMemcpyAsync(out + off, c->ubuf, n, cudaMemcpyDeviceToDevice, s));
+        if (cudaMemcpyAsync(c->ubuf, in + off, n, cudaMemcpyDeviceToDevice, s) != cudaSuccess) rc2 = T3DES_CU_ERR_CUDA;
+        if (!rc2) rc2 = run_device(c, dir, c->ubuf, c->ubuf, n / 8, s);
+        if (!rc2 && cudaMemcpyAsync(out + off, c->ubuf, n, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+            rc2 = T3DES_CU_ERR_CUDA;
     }
-    T3_CK(cudaStreamSynchronize(s));
-    return T3DES_CU_OK;
+    if (cudaStreamSynchronize(s) != cudaSuccess && !rc2) rc2 = T3DES_CU_ERR_CUDA;
+    if (rc2) (void)cudaGetLastError();
+    return rc2;
 }
 
 int t3des_cu_ecb_host(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8_t* out,
@@ -754,18 +768,21 @@ int t3des_cu_ecb_host(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uin
         }
         return n;
     };
+    // An error stops issuing but still waits for every stream: no queued D2H
+    // may write the caller's `out` after this call has returned.
     std::size_t k = 0;
-    for (std::size_t off = 0, n = 0; off < len; off += n, ++k) {
+    for (std::size_t off = 0, n = 0; off < len && !rc; off += n, ++k) {
         n = stage_bytes(k, len - off);
         cudaStream_t s = c->st[k % ns];
         std::uint8_t* b = c->buf[k % ns];
-        T3_CK(cudaMemcpyAsync(b, in + off, n, cudaMemcpyHostToDevice, s));
-        rc = run_device(c, dir, b, b, n / 8, s);
-        if (rc) return rc;
-        T3_CK(cudaMemcpyAsync(out + off, b, n, cudaMemcpyDeviceToHost, s));
+        if (cudaMemcpyAsync(b, in + off, n, cudaMemcpyHostToDevice, s) != cudaSuccess) rc = T3DES_CU_ERR_CUDA;
+        if (!rc) rc = run_device(c, dir, b, b, n / 8, s);
+        if (!rc && cudaMemcpyAsync(out + off, b, n, cudaMemcpyDeviceToHost, s) != cudaSuccess) rc = T3DES_CU_ERR_CUDA;
     }
-    for (int i = 0; i < ns; ++i) T3_CK(cudaStreamSynchronize(c->st[i]));
-    return T3DES_CU_OK;
+    for (int i = 0; i < ns; ++i)
+        if (cudaStreamSynchronize(c->st[i]) != cudaSuccess && !rc) rc = T3DES_CU_ERR_CUDA;
+    if (rc) (void)cudaGetLastError();
+    return rc;
 }
 
 int t3des_cu_set_pipeline(t3des_cu_ctx* c, std::size_t chunk_bytes, int streams) {
@@ -799,28 +816,74 @@ int t3des_cu_ecb_multi(const int* devices, int ndev, const std::uint64_t sub48[4
     if (partial_overlap(in, out, len)) return T3DES_CU_ERR_OVERLAP;
     if (!len) return T3DES_CU_OK;
     const std::uint64_t nblocks = len / 8;
+    // contexts first (pooled), so that each shard's host threads can be sized
+    // by how many shards share its device's NUMA node
+    std::vector<t3des_cu_ctx*> ctx(ndev, nullptr);
+    int rc = T3DES_CU_OK;
+    for (int g = 0; g < ndev && !rc; ++g) rc = pool_acquire(devices[g], &ctx[g]);
+    if (rc) {
+        for (auto* c : ctx) pool_release(c, true);
+        return rc;
+    }
+    const int hw = std::max(1, int(std::thread::hardware_concurrency()));
     std::vector<int> rcs(ndev, T3DES_CU_OK);
     std::vector<std::thread> workers;
     for (int g = 0; g < ndev; ++g) {
-        workers.emplace_back([&, g] {
+        t3des_cu_ctx* c = ctx[g];
+        c->numa_bind = true;  // pinned ring + copy threads on the device's node (a no-op where unknown)
+        if (!c->pool_in) {    // pageable spans: the host's copy threads are shared by the shards
+            int same = 0;
+            for (auto* o : ctx) same += o->numa.node == c->numa.node;
+            const int cpus = c->numa.node >= 0 ? int(c->numa.cpus.size()) : hw;
+            c->copy_threads = std::clamp(cpus / std::max(same, 1), 2, 12);
+        }
+        workers.emplace_back([&, g, c] {
             std::uint64_t b0 = 0, cnt = 0;
             t3des_cu_shard_range(nblocks, ndev, g, &b0, &cnt);
-            const std::uint64_t b1 = b0 + cnt;
-            if (b1 <= b0) return;
-            t3des_cu_ctx* c = nullptr;
-            int rc = pool_acquire(devices[g], &c);
-            // pageable spans: the host's copy threads are shared by the devices
-            if (!rc && !c->pool_in) c->copy_threads = std::max(2, int(std::thread::hardware_concurrency()) / ndev);
-            if (!rc) rc = t3des_cu_set_schedule(c, sub48);
-            if (!rc) rc = t3des_cu_ecb_host(c, dir, in + 8 * b0, out + 8 * b0, 8 * (b1 - b0));
-            pool_release(c, rc == T3DES_CU_OK || rc == T3DES_CU_ERR_ARG);
-            rcs[g] = rc;
+            if (!cnt) return;
+            t3b::NumaBind bind(c->numa);  // this shard's submitting thread next to its GPU
+            int r = t3des_cu_set_schedule(c, sub48);
+            if (!r) r = t3des_cu_ecb_host(c, dir, in + 8 * b0, out + 8 * b0, 8 * cnt);
+            rcs[g] = r;
         });
     }
     for (auto& w : workers) w.join();
-    for (int rc : rcs)
-        if (rc) return rc;
-    return T3DES_CU_OK;
+    for (int g = 0; g < ndev; ++g) {
+        pool_release(ctx[g], rcs[g] == T3DES_CU_OK || rcs[g] == T3DES_CU_ERR_ARG);
+        if (rcs[g] && !rc) rc = rcs[g];
+    }
+    return rc;
+}
+
+int t3des_cu_ecb_workers(unsigned workers, int first_device, const std::uint64_t sub48[48], int dir,
+                         const std::uint8_t* in, std::uint8_t* out, std::size_t len) {
+    if (!sub48 || (dir != 0 && dir != 1) || workers > 1024) return T3DES_CU_ERR_ARG;
+    if (len % 8) return T3DES_CU_ERR_LENGTH;
+    if (len && (!in || !out)) return T3DES_CU_ERR_ARG;
+    if (partial_overlap(in, out, len)) return T3DES_CU_ERR_OVERLAP;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n <= 0) {
+        (void)cudaGetLastError();
+        return T3DES_CU_ERR_NO_DEVICE;
+    }
+    if (first_device < 0 || first_device >= n) return T3DES_CU_ERR_NO_DEVICE;
+    if (!len) return T3DES_CU_OK;
+    const int w = workers == 0 ? 1 : int(workers);
+    if (w == 1) {
+        t3des_cu_ctx* c = nullptr;
+        int rc = pool_acquire(first_device, &c);
+        if (!rc && !c->pool_in) {
+            c->numa_bind = true;
+            if (c->numa.node >= 0) c->copy_threads = std::clamp(int(c->numa.cpus.size()) * 3 / 4, 2, 12);
+        }
+        if (!rc) rc = t3des_cu_set_schedule(c, sub48);
+        if (!rc) rc = t3des_cu_ecb_host(c, dir, in, out, len);
+        pool_release(c, rc == T3DES_CU_OK || rc == T3DES_CU_ERR_ARG);
+        return rc;
+    }
+    std::vector<int> devs(w);
+    for (int g = 0; g < w; ++g) devs[g] = (first_device + g) % n;
+    return t3des_cu_ecb_multi(devs.data(), w, sub48, dir, in, out, len);
 }
 
 int t3des_cu_ecb_multi_device(const int* devices, int ndev, const std::uint64_t sub48[48], int dir,
@@ -833,10 +896,18 @@ int t3des_cu_ecb_multi_device(const int* devices, int ndev, const std::uint64_t 
     const std::uint64_t nblocks = len / 8;
     const auto* in = static_cast<const std::uint8_t*>(din);
     auto* out = static_cast<std::uint8_t*>(dout);
+    const bool aligned = ((reinterpret_cast<std::uintptr_t>(in) | reinterpret_cast<std::uintptr_t>(out)) & 7u) == 0;
     std::vector<t3des_cu_ctx*> ctx(ndev, nullptr);
-    std::vector<std::uint8_t*> stage(ndev, nullptr);
     int rc = T3DES_CU_OK;
-    // issue every shard asynchronously on its device's stream, then wait
+    // Issue every shard asynchronously on its device, then wait.  A staged
+    // shard runs as a chunk pipeline over kStreams streams and staging
+    // buffers of its context: chunk k = peer copy in -> kernel -> peer copy
+    // out on stream k % kStreams, so chunk k's copy in overlaps chunk k-1's
+    // kernel and chunk k-2's copy out (NVLink both directions + SMs busy).
+    constexpr int kStreams = 3;
+    constexpr std::uint64_t kTileBytes = 8 * T3_TILE_BLOCKS;
+    std::uint64_t chunk_override = 0;
+    if (const char* e = std::getenv("T3DES_MULTI_CHUNK_BYTES")) chunk_override = std::strtoull(e, nullptr, 10);
     for (int g = 0; g < ndev && !rc; ++g) {
         std::uint64_t first = 0, count = 0;
         t3des_cu_shard_range(nblocks, ndev, g, &first, &count);
@@ -844,12 +915,11 @@ int t3des_cu_ecb_multi_device(const int* devices, int ndev, const std::uint64_t 
         rc = pool_acquire(devices[g], &ctx[g]);
         if (!rc) rc = t3des_cu_set_schedule(ctx[g], sub48);
         if (rc) break;
+        t3des_cu_ctx* c = ctx[g];
         DeviceScope scope(devices[g]);
-        cudaStream_t s = ctx[g]->st[0];
-        const std::size_t bytes = 8 * count;
-        const bool aligned = ((reinterpret_cast<std::uintptr_t>(in) | reinterpret_cast<std::uintptr_t>(out)) & 7u) == 0;
+        const std::uint64_t bytes = 8 * count;
         if (devices[g] == home && !(flags & T3DES_CU_MULTI_STAGE_ALL) && aligned) {
-            rc = run_device(ctx[g], dir, in + 8 * first, out + 8 * first, count, s);
+            rc = run_device(c, dir, in + 8 * first, out + 8 * first, count, c->st[0]);
             continue;
         }
         if (devices[g] != home) {
@@ -860,18 +930,30 @@ int t3des_cu_ecb_multi_device(const int* devices, int ndev, const std::uint64_t 
                 (void)cudaGetLastError();
             }
         }
-        if (!rc && cudaMalloc(&stage[g], bytes) != cudaSuccess) rc = T3DES_CU_ERR_CUDA;
-        if (!rc && cudaMemcpyPeerAsync(stage[g], devices[g], in + 8 * first, home, bytes, s) != cudaSuccess)
-            rc = T3DES_CU_ERR_CUDA;
-        if (!rc) rc = run_device(ctx[g], dir, stage[g], stage[g], count, s);
-        if (!rc && cudaMemcpyPeerAsync(out + 8 * first, home, stage[g], devices[g], bytes, s) != cudaSuccess)
-            rc = T3DES_CU_ERR_CUDA;
+        // chunk: about 1/8 of the shard, 8..256 MiB, whole warp tiles
+        std::uint64_t chunk =
+            std::clamp<std::uint64_t>(bytes / 8, std::uint64_t(8) << 20, std::uint64_t(256) << 20);
+        chunk -= chunk % kTileBytes;
+        if (chunk_override) chunk = std::max<std::uint64_t>(8, chunk_override - chunk_override % 8);  // tests
+        chunk = std::min(chunk, bytes);
+        if (!rc) rc = t3b::ensure_staging(c, chunk, kStreams);
+        std::uint64_t k = 0;
+        for (std::uint64_t off = 0; off < bytes && !rc; off += chunk, ++k) {
+            const std::uint64_t n = std::min(chunk, bytes - off);
+            cudaStream_t s = c->st[k % kStreams];
+            std::uint8_t* b = c->buf[k % kStreams];
+            if (cudaMemcpyPeerAsync(b, devices[g], in + 8 * first + off, home, n, s) != cudaSuccess)
+                rc = T3DES_CU_ERR_CUDA;
+            if (!rc) rc = run_device(c, dir, b, b, n / 8, s);
+            if (!rc && cudaMemcpyPeerAsync(out + 8 * first + off, home, b, devices[g], n, s) != cudaSuccess)
+                rc = T3DES_CU_ERR_CUDA;
+        }
     }
     for (int g = 0; g < ndev; ++g) {
         if (!ctx[g]) continue;
         DeviceScope scope(devices[g]);
-        if (cudaStreamSynchronize(ctx[g]->st[0]) != cudaSuccess && !rc) rc = T3DES_CU_ERR_CUDA;
-        if (stage[g]) cudaFree(stage[g]);
+        for (int i = 0; i < kStreams; ++i)
+            if (cudaStreamSynchronize(ctx[g]->st[i]) != cudaSuccess && !rc) rc = T3DES_CU_ERR_CUDA;
         pool_release(ctx[g], rc == T3DES_CU_OK || rc == T3DES_CU_ERR_ARG);
     }
     (void)cudaGetLastError();

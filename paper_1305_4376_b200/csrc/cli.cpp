@@ -355,30 +355,39 @@ int run_bench(const Opts& o) {
                 t3des_cu_ctx* c = nullptr;
                 int rc = t3des_cu_create(o.device, &c);
                 if (rc) throw std::runtime_error(t3des_cu_strerror(rc));
+                // buffers and timing events on the context's device (not the
+                // current one): the kernels run there
+                int prev_dev = 0;
+                cudaGetDevice(&prev_dev);
                 void *din = nullptr, *dout = nullptr;
-                cudaMalloc(&din, bytes);
-                cudaMalloc(&dout, bytes);
-                cudaMemcpy(din, payload.data(), bytes, cudaMemcpyHostToDevice);
-                rc = t3des_cu_set_schedule(c, sub48);
-                if (!rc) rc = t3des_cu_set_variant(c, make_config(o).variant);
-                if (!rc) rc = t3des_cu_set_launch(c, r.chunk, static_cast<int>(wg_arg));
-                cudaEvent_t e0, e1;
-                cudaEventCreate(&e0);
-                cudaEventCreate(&e1);
+                cudaEvent_t e0 = nullptr, e1 = nullptr;
+                auto ck = [&](cudaError_t e) {
+                    if (e != cudaSuccess && !rc) rc = T3DES_CU_ERR_CUDA;
+                    return rc == 0;
+                };
+                if (ck(cudaSetDevice(o.device)) && ck(cudaMalloc(&din, bytes)) && ck(cudaMalloc(&dout, bytes)) &&
+                    ck(cudaMemcpy(din, payload.data(), bytes, cudaMemcpyHostToDevice)) && ck(cudaEventCreate(&e0)) &&
+                    ck(cudaEventCreate(&e1))) {
+                    rc = t3des_cu_set_schedule(c, sub48);
+                    if (!rc) rc = t3des_cu_set_variant(c, make_config(o).variant);
+                    if (!rc) rc = t3des_cu_set_launch(c, r.chunk, static_cast<int>(wg_arg));
+                }
                 for (unsigned rep = 0; rep <= o.reps && !rc; ++rep) {  // rep 0 = warm-up
-                    cudaEventRecord(e0, nullptr);
-                    rc = t3des_cu_ecb_device(c, T3DES_CU_ENCRYPT, din, dout, bytes, nullptr);
-                    cudaEventRecord(e1, nullptr);
-                    cudaEventSynchronize(e1);
+                    ck(cudaEventRecord(e0, nullptr));
+                    if (!rc) rc = t3des_cu_ecb_device(c, T3DES_CU_ENCRYPT, din, dout, bytes, nullptr);
+                    ck(cudaEventRecord(e1, nullptr));
+                    ck(cudaEventSynchronize(e1));
                     float ms = 0;
-                    cudaEventElapsedTime(&ms, e0, e1);
+                    ck(cudaEventElapsedTime(&ms, e0, e1));
                     if (rep > 0 && (rep == 1 || ms * 1e-3 < best)) best = ms * 1e-3;
                 }
-                if (!rc) rc = cudaMemcpy(out.data(), dout, bytes, cudaMemcpyDeviceToHost) ? T3DES_CU_ERR_CUDA : 0;
-                cudaEventDestroy(e0);
-                cudaEventDestroy(e1);
-                cudaFree(din);
-                cudaFree(dout);
+                if (!rc) ck(cudaMemcpy(out.data(), dout, bytes, cudaMemcpyDeviceToHost));
+                if (e0) cudaEventDestroy(e0);
+                if (e1) cudaEventDestroy(e1);
+                if (din) cudaFree(din);
+                if (dout) cudaFree(dout);
+                (void)cudaGetLastError();
+                cudaSetDevice(prev_dev);
                 t3des_cu_destroy(c);
                 if (rc) throw std::runtime_error(t3des_cu_strerror(rc));
             } else {
@@ -396,6 +405,7 @@ int run_bench(const Opts& o) {
             }
             // every record must decrypt back and agree with the first record
             t3des::DispatchConfig chk;
+            chk.device = o.device;
             t3des::decrypt_batch(out, back, ts, chk);
             if (back != payload) throw std::runtime_error("round trip mismatch");
             if (first_ct.empty()) first_ct = out;

@@ -13,9 +13,7 @@
 #endif
 #include "t3des_cu.h"
 
-namespace t3b {
-class CopyPool;
-}
+#include "hoststage.hpp"
 
 struct t3des_cu_ctx {
     int device = 0;
@@ -53,10 +51,13 @@ struct t3des_cu_ctx {
     std::size_t hbuf_bytes = 0;
     cudaEvent_t hev[kHostSlots] = {};
     bool hev_live[kHostSlots] = {};
+    bool hbuf_registered[kHostSlots] = {};  // allocated by host_alloc_on_node (mmap + register)
     t3b::CopyPool* pool_in = nullptr;
     t3b::CopyPool* pool_out = nullptr;
     std::size_t stage_bytes = std::size_t(4) << 20;  // pageable stage size
     int copy_threads = 0;                            // total host copy threads (0 = auto)
+    t3b::NumaNode numa;      // the device's NUMA node (node -1: unknown / single-node host)
+    bool numa_bind = false;  // place pinned staging and copy threads on `numa` (multi-GPU contexts)
     std::uint32_t* d_spk = nullptr;  // device copies of sp[2], sp16[2] (48 x 8 words each)
     std::uint8_t* ubuf = nullptr;  // bounce buffer for device spans that are not 8-byte aligned
     std::uint64_t launches = 0;
@@ -65,6 +66,22 @@ struct t3des_cu_ctx {
 };
 
 namespace t3b {
+
+// Makes `dev` the current device and restores the caller's on scope exit.
+// Every entry point that allocates, launches or synchronises on a context's
+// resources opens one (streams, events and buffers belong to c->device).
+struct DeviceScope {
+    int prev = -1;
+    explicit DeviceScope(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        cudaSetDevice(dev);
+    }
+    ~DeviceScope() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+    DeviceScope(const DeviceScope&) = delete;
+    DeviceScope& operator=(const DeviceScope&) = delete;
+};
 
 // Transform nblocks device blocks on stream s (in may equal out), honouring
 // the context's variant and launch shaping.  Returns a T3DES_CU_* status.

@@ -1,9 +1,19 @@
 // Host copy pool for the pageable staging path (hoststage.hpp).
 #include "hoststage.hpp"
 
+#include <cuda_runtime.h>
+#include <pthread.h>
+#include <sched.h>
+#include <sys/mman.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
 #include <algorithm>
+#include <cctype>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 #if defined(__x86_64__)
 #include <emmintrin.h>
 #endif
@@ -46,9 +56,145 @@ void stream_copy(char* d, const char* s, std::size_t n) {
     std::memcpy(d, s, n);
 }
 
+constexpr int kMpolDefault = 0, kMpolPreferred = 1, kMpolBind = 2;  // linux/mempolicy.h
+constexpr unsigned long kMaxNode = 1024;                            // bits in the masks below
+
+std::string sysfs_root() {
+    const char* e = std::getenv("T3DES_SYSFS_ROOT");
+    return e ? e : "/sys";
+}
+
+bool read_line(const std::string& path, std::string& out) {
+    std::FILE* f = std::fopen(path.c_str(), "r");
+    if (!f) return false;
+    char buf[4096];
+    const bool ok = std::fgets(buf, sizeof buf, f) != nullptr;
+    std::fclose(f);
+    if (!ok) return false;
+    out = buf;
+    while (!out.empty() && std::isspace(static_cast<unsigned char>(out.back()))) out.pop_back();
+    return true;
+}
+
+int count_nodes(const std::string& root) {
+    int n = 0;
+    for (int k = 0; k < 1024; ++k) {
+        std::string tmp;
+        if (read_line(root + "/devices/system/node/node" + std::to_string(k) + "/cpulist", tmp)) ++n;
+        else if (k > 64 && n) break;
+    }
+    return n;
+}
+
 }  // namespace
 
-CopyPool::CopyPool(int nthreads) : n_(std::max(1, nthreads)) {
+std::vector<int> parse_cpulist(const char* s) {
+    std::vector<int> cpus;
+    if (!s) return cpus;
+    const char* p = s;
+    while (*p) {
+        char* end = nullptr;
+        const long a = std::strtol(p, &end, 10);
+        if (end == p || a < 0) return {};
+        long b = a;
+        p = end;
+        if (*p == '-') {
+            ++p;
+            b = std::strtol(p, &end, 10);
+            if (end == p || b < a) return {};
+            p = end;
+        }
+        for (long c = a; c <= b && c < 65536; ++c) cpus.push_back(int(c));
+        if (*p == ',') ++p;
+        else if (*p && !std::isspace(static_cast<unsigned char>(*p))) return {};
+        else if (*p) break;
+    }
+    return cpus;
+}
+
+NumaNode numa_node_of_pci(const char* bus_id) {
+    NumaNode n;
+    if (const char* e = std::getenv("T3DES_NUMA"); e && std::atoi(e) == 0) return n;
+    if (!bus_id) return n;
+    std::string id(bus_id);
+    for (auto& ch : id) ch = char(std::tolower(static_cast<unsigned char>(ch)));
+    const std::string root = sysfs_root();
+    std::string v;
+    if (!read_line(root + "/bus/pci/devices/" + id + "/numa_node", v)) return n;
+    const int node = std::atoi(v.c_str());
+    if (node < 0 || count_nodes(root) < 2) return n;
+    if (!read_line(root + "/devices/system/node/node" + std::to_string(node) + "/cpulist", v)) return n;
+    cpu_set_t allowed;
+    CPU_ZERO(&allowed);
+    const bool have_mask = sched_getaffinity(0, sizeof allowed, &allowed) == 0;
+    for (int c : parse_cpulist(v.c_str()))
+        if (!have_mask || (c < CPU_SETSIZE && CPU_ISSET(c, &allowed))) n.cpus.push_back(c);
+    if (!n.cpus.empty()) n.node = node;
+    return n;
+}
+
+NumaBind::NumaBind(const NumaNode& n) {
+    if (n.node < 0 || n.cpus.empty()) return;
+    static_assert(sizeof(cpu_set_t) <= sizeof old_cpus_, "cpu_set_t storage");
+    auto* old = reinterpret_cast<cpu_set_t*>(old_cpus_);
+    if (pthread_getaffinity_np(pthread_self(), sizeof(cpu_set_t), old) == 0) {
+        cpu_set_t set;
+        CPU_ZERO(&set);
+        for (int c : n.cpus)
+            if (c < CPU_SETSIZE) CPU_SET(c, &set);
+        cpus_bound_ = pthread_setaffinity_np(pthread_self(), sizeof set, &set) == 0;
+    }
+    unsigned long mask[kMaxNode / (8 * sizeof(unsigned long))] = {};
+    if (n.node < int(kMaxNode)) {
+        mask[n.node / (8 * sizeof(unsigned long))] |= 1ul << (n.node % (8 * sizeof(unsigned long)));
+        if (syscall(SYS_get_mempolicy, &old_mode_, old_mask_, kMaxNode, nullptr, 0ul) == 0)
+            policy_set_ = syscall(SYS_set_mempolicy, kMpolPreferred, mask, kMaxNode) == 0;
+    }
+}
+
+NumaBind::~NumaBind() {
+    if (cpus_bound_) pthread_setaffinity_np(pthread_self(), sizeof(cpu_set_t), reinterpret_cast<cpu_set_t*>(old_cpus_));
+    if (policy_set_) {
+        if (old_mode_ == kMpolDefault) syscall(SYS_set_mempolicy, kMpolDefault, nullptr, 0ul);
+        else syscall(SYS_set_mempolicy, old_mode_, old_mask_, kMaxNode);
+    }
+}
+
+int host_alloc_on_node(std::size_t bytes, const NumaNode& n, void** out, bool* registered) {
+    *out = nullptr;
+    *registered = false;
+    if (n.node < 0 || n.node >= int(kMaxNode)) {
+        const cudaError_t e = cudaMallocHost(out, bytes);
+        return int(e);
+    }
+    void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (p == MAP_FAILED) return int(cudaErrorMemoryAllocation);
+    unsigned long mask[kMaxNode / (8 * sizeof(unsigned long))] = {};
+    mask[n.node / (8 * sizeof(unsigned long))] |= 1ul << (n.node % (8 * sizeof(unsigned long)));
+    (void)syscall(SYS_mbind, p, bytes, kMpolBind, mask, kMaxNode, 0u);  // best effort: placement, not correctness
+    std::memset(p, 0, bytes);                                         // fault the pages in on that node
+    const cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        munmap(p, bytes);
+        return int(e);
+    }
+    *out = p;
+    *registered = true;
+    return 0;
+}
+
+void host_free_on_node(void* p, std::size_t bytes, bool registered) {
+    if (!p) return;
+    if (registered) {
+        cudaHostUnregister(p);
+        munmap(p, bytes);
+    } else {
+        cudaFreeHost(p);
+    }
+}
+
+CopyPool::CopyPool(int nthreads, NumaNode node) : n_(std::max(1, nthreads)), node_(std::move(node)) {
     th_.reserve(n_);
     for (int i = 0; i < n_; ++i) th_.emplace_back([this, i] { run(i); });
 }
@@ -86,6 +232,7 @@ void CopyPool::wait() {
 }
 
 void CopyPool::run(int i) {
+    NumaBind bind(node_);  // for the thread's lifetime
     std::uint64_t seen = 0;
     for (;;) {
         char* d;

@@ -17,11 +17,54 @@
 
 namespace t3b {
 
+// NUMA placement of one device's host-side work (multi-GPU end
+// to end): the CPUs and memory node local to the GPU's PCIe root.  node < 0:
+// unknown, or a single-node host (nothing to place).
+struct NumaNode {
+    int node = -1;
+    std::vector<int> cpus;  // the node's CPUs that this process may run on
+};
+
+// "0-3,8,10-11" -> {0,1,2,3,8,10,11}; malformed input -> {}.
+std::vector<int> parse_cpulist(const char* s);
+
+// The NUMA node of a PCI device ("0000:1B:00.0", any case) from sysfs
+// (/sys/bus/pci/devices/<id>/numa_node, /sys/devices/system/node/node<k>/
+// cpulist; root overridable with T3DES_SYSFS_ROOT for tests).  Returns
+// node -1 on single-node hosts, when sysfs has no answer, or with
+// T3DES_NUMA=0.
+NumaNode numa_node_of_pci(const char* bus_id);
+
+// Binds the calling thread to a node's CPUs and makes that node its
+// preferred memory node; restores both on destruction.  No-op for node < 0.
+class NumaBind {
+public:
+    explicit NumaBind(const NumaNode& n);
+    ~NumaBind();
+    NumaBind(const NumaBind&) = delete;
+    NumaBind& operator=(const NumaBind&) = delete;
+    bool active() const { return cpus_bound_; }
+
+private:
+    bool cpus_bound_ = false, policy_set_ = false;
+    int old_mode_ = 0;
+    unsigned long old_mask_[16] = {};
+    unsigned char old_cpus_[128] = {};  // cpu_set_t storage
+};
+
+// Page-locked host memory on a NUMA node: mmap + mbind(MPOL_BIND) + first
+// touch + cudaHostRegister (mapped, portable), so the pages are where the
+// device's DMA and copy threads are.  node < 0 falls back to cudaMallocHost.
+// Returns 0 or a cudaError_t value.
+int host_alloc_on_node(std::size_t bytes, const NumaNode& n, void** out, bool* registered);
+void host_free_on_node(void* p, std::size_t bytes, bool registered);
+
 // A fixed set of threads that split one memcpy at a time between them.
 // start() hands out a job and returns; wait() blocks until it is done.
 class CopyPool {
 public:
-    explicit CopyPool(int nthreads);
+    // threads are bound to `node`'s CPUs when it is known
+    explicit CopyPool(int nthreads, NumaNode node = {});
     ~CopyPool();
     CopyPool(const CopyPool&) = delete;
     CopyPool& operator=(const CopyPool&) = delete;
@@ -34,6 +77,7 @@ public:
 private:
     void run(int i);
     const int n_;
+    const NumaNode node_;
     std::mutex m_;
     std::condition_variable cv_, done_cv_;
     std::uint64_t gen_ = 0;

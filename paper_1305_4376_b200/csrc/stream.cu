@@ -76,6 +76,7 @@ std::size_t pkcs7_unpad_len(const std::uint8_t* data, std::size_t len) {
 
 StreamStats run_stream(t3des_cu_ctx* c, int dir, ByteSource& src, ByteSink& dst, std::size_t chunk_blocks,
                        bool pkcs7) {
+    DeviceScope scope(c->device);  // the ring, staging and streams live on the context's device
     StreamStats st;
     const std::size_t chunk = chunk_blocks * 8;
     const bool enc = dir == T3DES_CU_ENCRYPT;

@@ -69,12 +69,9 @@ void run_batch(std::span<const std::uint8_t> in, std::span<std::uint8_t> out, co
     if (in.empty()) return;
     std::uint64_t sub48[48];
     flatten(ts, sub48);
-    const unsigned ngpu = cfg.workers == 0 ? 1u : cfg.workers;
     int rc;
-    if (ngpu > 1) {
-        std::vector<int> devs(ngpu);
-        for (unsigned g = 0; g < ngpu; ++g) devs[g] = cfg.device + static_cast<int>(g);
-        rc = t3des_cu_ecb_multi(devs.data(), static_cast<int>(ngpu), sub48, dir, ib, out.data(), in.size());
+    if (cfg.workers > 1) {  // shards round-robin over the visible GPUs from cfg.device
+        rc = t3des_cu_ecb_workers(cfg.workers, cfg.device, sub48, dir, ib, out.data(), in.size());
     } else {
         t3des_cu_ctx* c = context_for(cfg.device);
         rc = t3des_cu_set_schedule(c, sub48);

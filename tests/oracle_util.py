@@ -45,6 +45,8 @@ class Oracle:
         lib.oracle_splitmix_payload.argtypes = [_vp, U64, _sz, U64]
         lib.oracle_splitmix_block.argtypes = [U64, U64]
         lib.oracle_splitmix_block.restype = U64
+        lib.oracle_checksum.argtypes = [_vp, U64, _sz]
+        lib.oracle_checksum.restype = U64
         lib.oracle_tdes_block.argtypes = [U64, ctypes.POINTER(U64), ctypes.c_int]
         lib.oracle_tdes_block.restype = U64
         lib.oracle_des_block.argtypes = [U64, U64, ctypes.c_int]
@@ -98,6 +100,11 @@ class Oracle:
         buf = np.empty(max(8 * nblocks, 8), dtype=np.uint8)
         self.lib.oracle_splitmix_payload(_ptr(buf), first_block, nblocks, seed)
         return buf[: 8 * nblocks]
+
+    def checksum(self, data: np.ndarray, first_block: int = 0) -> int:
+        """oracle_checksum: the C restatement of t3_checksum_kernel."""
+        assert data.nbytes % 8 == 0
+        return int(self.lib.oracle_checksum(_ptr(data), first_block, data.nbytes // 8))
 
     def ref_ecb(self, data: np.ndarray, sub48, decrypt: int, backend: int = 1, workers: int = 0) -> np.ndarray:
         assert self.ref is not None

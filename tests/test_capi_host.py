@@ -99,6 +99,12 @@ def test_c_abi_status_codes(engine_lib):
     keys = (ctypes.c_uint64 * 3)()
     assert L.t3des_cu_parse_hex_key(b"00", 2, keys, None) == N.ERR_KEY
     assert L.t3des_cu_ecb_device(None, 0, None, None, 0, None) == N.ERR_ARG
+    sub = (ctypes.c_uint64 * 48)()
+    buf = ctypes.create_string_buffer(24)
+    assert L.t3des_cu_ecb_workers(2, 0, None, 0, buf, buf, 16) == N.ERR_ARG
+    assert L.t3des_cu_ecb_workers(2, 0, sub, 2, buf, buf, 16) == N.ERR_ARG
+    assert L.t3des_cu_ecb_workers(2, 0, sub, 0, buf, buf, 12) == N.ERR_LENGTH
+    assert L.t3des_cu_ecb_workers(2, 0, sub, 0, ctypes.addressof(buf), ctypes.addressof(buf) + 8, 16) == N.ERR_OVERLAP
 
 
 @pytest.mark.skipif("__import__('torch').cuda.is_available()")
@@ -108,6 +114,8 @@ def test_no_device_is_an_error_not_a_fallback(engine_lib):
     ts = t3.triple_schedule(t3.parse_hex_key("0123456789ABCDEF"))
     with pytest.raises(t3.CudaError):
         t3.encrypt_batch(b"\0" * 64, bytearray(64), ts)
+    with pytest.raises(t3.CudaError):  # the workers axis too
+        t3.encrypt_batch(b"\0" * 64, bytearray(64), ts, t3.DispatchConfig(workers=2))
 
 
 def test_cpp_api_compiles_and_reports_errors(engine_lib, tmp_path):

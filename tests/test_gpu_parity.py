@@ -474,6 +474,49 @@ def test_multi_device_resident_scatter_gather(oracle):
     assert rc == 0 and np.array_equal(b[5: 5 + x.nbytes].cpu().numpy(), oracle.ecb(x, s, 0))
 
 
+@pytest.mark.parametrize("chunk_bytes,n", [(8 * 1000 + 8, 3 * 1024 * 9 + 5), (None, (72 << 20) // 8 + 13)])
+def test_multi_device_chunk_pipeline(oracle, monkeypatch, chunk_bytes, n):
+    """ecb_multi_device with STAGE_ALL: every shard runs as a chunk pipeline
+    (peer copy in -> kernel -> peer copy out on three streams); ragged chunk
+    sizes (not whole tiles) and the default 8 MiB+ chunking, both directions."""
+    if chunk_bytes:
+        monkeypatch.setenv("T3DES_MULTI_CHUNK_BYTES", str(chunk_bytes))
+    ngpu = torch.cuda.device_count()
+    devs = list(range(ngpu)) if ngpu > 1 else [0, 0, 0]
+    s = oracle.schedule_hex(KEYS[1])
+    x = oracle.splitmix(0, n, 0xABC)
+    src = dev(x)
+    dst = torch.empty_like(src)
+    arr = (ctypes.c_int * len(devs))(*devs)
+    rc = N.lib().t3des_cu_ecb_multi_device(arr, len(devs), s, 0, 0, src.data_ptr(), dst.data_ptr(), x.nbytes, 1)
+    assert rc == 0
+    assert np.array_equal(host(dst), oracle.ecb(x, s, 0))
+    rc = N.lib().t3des_cu_ecb_multi_device(arr, len(devs), s, 1, 0, dst.data_ptr(), dst.data_ptr(), x.nbytes, 1)
+    assert rc == 0 and torch.equal(dst, src)
+
+
+@pytest.mark.parametrize("workers", [0, 1, 2, 3])
+def test_workers_axis(oracle, workers):
+    """t3des_cu_ecb_workers — DispatchConfig.workers on the GPU: that many
+    block-range shards round-robin over the visible GPUs (two or three
+    contexts on one GPU here), pageable and pinned spans; the Python API
+    routes cfg.workers > 1 through it."""
+    s = oracle.schedule_hex(KEYS[0])
+    x = oracle.payload(8 * (5 * 1024 * 7 + 3))
+    y = np.empty_like(x)
+    rc = N.lib().t3des_cu_ecb_workers(workers, 0, s, 0, x.ctypes.data, y.ctypes.data, x.nbytes)
+    assert rc == 0 and np.array_equal(y, oracle.ecb(x, s, 0))
+    pinned = torch.from_numpy(y).pin_memory()
+    rc = N.lib().t3des_cu_ecb_workers(workers, 0, s, 1, pinned.data_ptr(), pinned.data_ptr(), x.nbytes)
+    assert rc == 0 and np.array_equal(pinned.numpy(), x)
+    ts = t3.triple_schedule(t3.parse_hex_key(KEYS[0]))
+    out = np.empty_like(x)
+    t3.encrypt_batch(x, out, ts, t3.DispatchConfig(workers=workers))
+    assert np.array_equal(out, y)
+    assert N.lib().t3des_cu_ecb_workers(2, torch.cuda.device_count(), s, 0, x.ctypes.data, y.ctypes.data,
+                                        x.nbytes) == N.ERR_NO_DEVICE
+
+
 def test_auto_variant_with_large_work_group(eng, oracle):
     """AUTO + a 256-thread work group: small launches use it on the SP-table
     kernel, large ones clamp it to the bitsliced kernel's 128 threads."""
