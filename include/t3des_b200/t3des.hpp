@@ -115,6 +115,21 @@ void encrypt_batch(std::span<const std::uint8_t> in, std::span<std::uint8_t> out
 void decrypt_batch(std::span<const std::uint8_t> in, std::span<std::uint8_t> out,
                    const TripleSchedule& ts, const DispatchConfig& cfg);
 
+// Opt-in page-locking of a buffer the caller passes to many batch calls
+// (t3des_cu_host_register): the host path then DMAs straight from/to it
+// instead of staging it.  RAII: unregisters on destruction, which must come
+// before the memory is freed.
+class HostRegistration {
+  public:
+    explicit HostRegistration(std::span<std::uint8_t> buf);
+    ~HostRegistration();
+    HostRegistration(const HostRegistration&) = delete;
+    HostRegistration& operator=(const HostRegistration&) = delete;
+
+  private:
+    void* p_ = nullptr;
+};
+
 enum class PaddingMode { None, Pkcs7 };
 
 struct StreamReport {

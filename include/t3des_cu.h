@@ -195,6 +195,17 @@ int t3des_cu_stream_fd(t3des_cu_ctx* ctx, int direction, int in_fd, int out_fd, 
 int t3des_cu_host_alloc(size_t bytes, void** out);
 int t3des_cu_host_free(void* p);
 
+/* Opt-in page-locking of a caller's existing (pageable) buffer, for callers
+ * that pass the same std::vector / array to many batch calls: once
+ * registered, t3des_cu_ecb_host DMAs straight from/to it (the pinned path,
+ * PCIe-bound) instead of staging it through the engine's pinned ring (host-
+ * DRAM-bound, about half the rate).  Registration itself costs about as much
+ * as one staged transform of the buffer, so it pays from the second call on.
+ * The caller must unregister before freeing the memory.  Never done
+ * implicitly: a freed-and-reused address would keep stale pages pinned. */
+int t3des_cu_host_register(void* p, size_t bytes);
+int t3des_cu_host_unregister(void* p);
+
 /* Device payload generator for inputs larger than host RAM: block
  * (first_block + i) = splitmix64(seed ^ (first_block + i)), big-endian. */
 int t3des_cu_fill_splitmix(t3des_cu_ctx* ctx, void* dptr, uint64_t first_block, size_t nblocks,

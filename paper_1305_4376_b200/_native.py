@@ -70,6 +70,8 @@ SIGNATURES = {
     "t3des_cu_shard_range": (_i, [ctypes.c_uint64, _i, _i, _u64p, _u64p]),
     "t3des_cu_host_alloc": (_i, [_sz, ctypes.POINTER(_vp)]),
     "t3des_cu_host_free": (_i, [_vp]),
+    "t3des_cu_host_register": (_i, [_vp, _sz]),
+    "t3des_cu_host_unregister": (_i, [_vp]),
     "t3des_cu_fill_splitmix": (_i, [_vp, _vp, ctypes.c_uint64, _sz, ctypes.c_uint64, _vp]),
     "t3des_cu_checksum": (_i, [_vp, _vp, ctypes.c_uint64, _sz, _u64p, _vp]),
     "t3des_cu_launch_count": (_i, [_vp, _u64p]),

@@ -342,6 +342,33 @@ def _run_batch(src, dst, ts: TripleSchedule, cfg: DispatchConfig, direction: int
     del keep_in, keep_out
 
 
+class HostRegistration:
+    """Opt-in page-locking of a host buffer passed to many batch calls
+    (t3des_cu_host_register): the host path then DMAs straight from/to it
+    instead of staging it through the engine's pinned ring.  Use as a context
+    manager, or call close(); it must be closed before the buffer is freed."""
+
+    def __init__(self, buf):
+        p, n, keep = _host_view(buf, False)
+        self._keep = keep
+        self._p = None
+        if n:
+            _raise(N.lib().t3des_cu_host_register(p, n), "host register")
+            self._p = p
+
+    def close(self) -> None:
+        if self._p is not None:
+            _raise(N.lib().t3des_cu_host_unregister(self._p), "host unregister")
+            self._p = None
+            self._keep = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
 def encrypt_batch(src, dst, ts: TripleSchedule, cfg: DispatchConfig | None = None) -> None:
     """ECB-encrypt `src` into `dst` (same length, multiple of 8 bytes;
     in place allowed, partial overlap rejected)."""

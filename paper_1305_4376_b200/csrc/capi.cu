@@ -972,6 +972,24 @@ int t3des_cu_host_free(void* p) {
     return T3DES_CU_OK;
 }
 
+int t3des_cu_host_register(void* p, std::size_t bytes) {
+    if (!p || !bytes) return T3DES_CU_ERR_ARG;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n <= 0) {
+        (void)cudaGetLastError();
+        return T3DES_CU_ERR_NO_DEVICE;
+    }
+    // portable: pinned for every context; mapped: the zero-copy small-batch path applies too
+    T3_CK(cudaHostRegister(p, bytes, cudaHostRegisterPortable | cudaHostRegisterMapped));
+    return T3DES_CU_OK;
+}
+
+int t3des_cu_host_unregister(void* p) {
+    if (!p) return T3DES_CU_ERR_ARG;
+    T3_CK(cudaHostUnregister(p));
+    return T3DES_CU_OK;
+}
+
 int t3des_cu_fill_splitmix(t3des_cu_ctx* c, void* dptr, std::uint64_t first_block, std::size_t nblocks,
                            std::uint64_t seed, void* stream) {
     if (!c || (nblocks && !dptr)) return T3DES_CU_ERR_ARG;

@@ -143,6 +143,16 @@ StreamReport decrypt_stream(std::istream& source, std::ostream& sink, const Trip
     return run_stream(source, sink, ts, cfg, pad, T3DES_CU_DECRYPT);
 }
 
+HostRegistration::HostRegistration(std::span<std::uint8_t> buf) {
+    if (buf.empty()) return;
+    if (int rc = t3des_cu_host_register(buf.data(), buf.size())) raise(rc);
+    p_ = buf.data();
+}
+
+HostRegistration::~HostRegistration() {
+    if (p_) t3des_cu_host_unregister(p_);
+}
+
 void pkcs7_pad(std::vector<std::uint8_t>& data) {
     const std::size_t len = data.size();
     data.resize(len + 8 - len % 8);

@@ -517,6 +517,25 @@ def test_workers_axis(oracle, workers):
                                         x.nbytes) == N.ERR_NO_DEVICE
 
 
+def test_host_registration_of_pageable_buffers(oracle):
+    """Opt-in t3des_cu_host_register: a registered numpy buffer takes the
+    pinned DMA path (no staging); results equal the oracle; unregistering
+    returns it to the staged path; the C++ RAII type is in the library."""
+    ts = t3.triple_schedule(t3.parse_hex_key(KEYS[0]))
+    s = oracle.schedule_hex(KEYS[0])
+    x = oracle.payload(8 * ((3 << 20) + 5))
+    y = np.empty_like(x)
+    with t3.HostRegistration(x), t3.HostRegistration(y):
+        t3.encrypt_batch(x, y, ts)
+        assert np.array_equal(y, oracle.ecb(x, s, 0))
+        t3.decrypt_batch(y, y, ts)  # in place on a registered buffer
+        assert np.array_equal(y, x)
+    t3.encrypt_batch(x, y, ts)  # unregistered again: staged path
+    assert np.array_equal(y, oracle.ecb(x, s, 0))
+    assert N.lib().t3des_cu_host_unregister(x.ctypes.data) == N.ERR_CUDA  # not registered any more
+    assert N.lib().t3des_cu_host_register(None, 8) == N.ERR_ARG
+
+
 def test_auto_variant_with_large_work_group(eng, oracle):
     """AUTO + a 256-thread work group: small launches use it on the SP-table
     kernel, large ones clamp it to the bitsliced kernel's 128 threads."""
