@@ -83,3 +83,18 @@ def test_cli_smoke_on_device(cli, oracle, tmp_path):
     assert lines[0] == ("backend,workers,chunk_blocks,work_group,payload_bytes,compute_seconds,io_seconds,"
                         "throughput_mb_s,speedup_vs_baseline,ok")
     assert len(lines) == 3 and all(l.endswith(",ok") for l in lines[1:])
+
+
+@pytest.mark.gpu
+def test_cli_bench_device_mode_on_last_device(cli, tmp_path):
+    """`bench --mode device --device D` allocates, times and checks on device
+    D (it used to allocate on the current device)."""
+    import torch
+
+    d = torch.cuda.device_count() - 1
+    out = tmp_path / "b.csv"
+    p = run(cli, "bench", "--mode", "device", "--device", str(d), "--sweep", "chunk", "--values", "0,65536",
+            "--payload-mb", "8", "--reps", "1", "--format", "csv", "--out", str(out), timeout=300)
+    assert p.returncode == 0, p.stderr
+    rows = out.read_text().strip().splitlines()[1:]
+    assert len(rows) == 2 and all(r.split(",")[-1] == "ok" for r in rows), rows

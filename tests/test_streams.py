@@ -198,3 +198,18 @@ def test_cpp_streams_on_device(engine_lib, oracle, tmp_path):
     assert p.returncode == 0, p.stderr
     want = oracle.ecb(np.frombuffer(b"a" * (1 << 20), np.uint8), oracle.schedule_hex(KEY), 0).tobytes()
     assert p.stdout == want
+
+
+@pytest.mark.gpu
+def test_stream_on_a_non_current_device(ts, oracle):
+    """encrypt_stream on device D while the caller's current device is 0: the
+    stream path opens a device scope.  Needs two GPUs."""
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs a second GPU")
+    torch.cuda.set_device(0)
+    payload = np.random.default_rng(49).integers(0, 256, 5000, dtype=np.uint8).tobytes()
+    mid = io.BytesIO()
+    t3.encrypt_stream(io.BytesIO(payload), mid, ts, t3.DispatchConfig(device=1, chunk_blocks=100), t3.PaddingMode.PKCS7)
+    assert mid.getvalue() == oracle.ecb(np.frombuffer(t3.pkcs7_pad(payload), np.uint8), oracle.schedule_hex(KEY), 0).tobytes()
