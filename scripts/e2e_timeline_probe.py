@@ -58,9 +58,54 @@ def make(kind):
     return run
 
 
+def split_run(R, kind="bitslice"):
+    """H2D stream, kernel stream, D2H stream chained by events over a ring
+    of R buffers (buffer j reused only after its D2H)."""
+    s_in, s_k, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    ring = [torch.empty(C, dtype=torch.uint8, device="cuda") for _ in range(R)]
+
+    def run():
+        ev_in = [torch.cuda.Event() for _ in range(R)]
+        ev_k = [torch.cuda.Event() for _ in range(R)]
+        ev_out = [torch.cuda.Event() for _ in range(R)]
+        used = [False] * R
+        for k, off in enumerate(range(0, nbytes, C)):
+            n = min(C, nbytes - off)
+            j = k % R
+            b = ring[j][:n]
+            if used[j]:
+                s_in.wait_event(ev_out[j])
+            with torch.cuda.stream(s_in):
+                b.copy_(h[off:off + n], non_blocking=True)
+                ev_in[j].record(s_in)
+            s_k.wait_event(ev_in[j])
+            if kind != "none":
+                e.set_variant(t3.VARIANT_BITSLICE)
+                e.ecb_device(0, b.data_ptr(), b.data_ptr(), n, s_k.cuda_stream)
+            ev_k[j].record(s_k)
+            s_out.wait_event(ev_k[j])
+            with torch.cuda.stream(s_out):
+                h[off:off + n].copy_(b, non_blocking=True)
+                ev_out[j].record(s_out)
+            used[j] = True
+    return run
+
+
 def main():
     nst = (nbytes + C - 1) // C
     out = {}
+    for R in (3, 4, 6):
+        for kind in ("none", "bitslice"):
+            run = split_run(R, kind)
+            run()
+            torch.cuda.synchronize()
+            best = 1e9
+            for _ in range(4):
+                t0 = time.perf_counter()
+                run()
+                torch.cuda.synchronize()
+                best = min(best, time.perf_counter() - t0)
+            print(f"split R={R} {kind}", json.dumps({"GBps": round(nbytes / best / 1e9, 2)}), flush=True)
     for kind in ("none", "torch", "bitslice", "sptable"):
         run = make(kind)
         run()
