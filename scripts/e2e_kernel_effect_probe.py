@@ -77,7 +77,7 @@ def run(kind):
 
 
 def main():
-    for kind in ("none", "sleep", "bitslice", "bs_oop", "bs_grid1", "torch", "none", "bitslice"):
+    for kind in ["none", "sleep", "bitslice", "bs_oop", "bs_grid1", "torch"] * 3:
         run(kind)
         torch.cuda.synchronize()
         best = 1e9
