@@ -569,6 +569,13 @@ def main() -> None:
     if world != args.gpus:
         print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
         sys.exit(2)
+    if os.environ.get("T3DES_BENCH_LAUNCH_PROBE"):  # tests: the launcher only, no work
+        from paper_1305_4376_b200.sharding import shard_range
+
+        n = ((args.gib if world == 1 else args.c3_gib) << 30) // 8
+        print(json.dumps({"rank": rank, "world": world, "local_rank": local, "shard": shard_range(n, world, rank)}),
+              flush=True)
+        return
     if args.impl == "reference":
         run_reference_impl(args, rank, world)
         return

@@ -90,3 +90,29 @@ def test_shard_range_properties():
     assert shard_range(8_589_934_592, 8, 3) == (3 * 1_073_741_824, 1_073_741_824)
     with pytest.raises(ValueError):
         shard_range(10, 2, 2)
+
+
+def test_bench_self_launches_n_ranks():
+    """`bench.py --gpus 2` outside torchrun re-launches itself under
+    torch.distributed.run with 2 ranks (T3DES_BENCH_LAUNCH_PROBE: the ranks
+    report and exit before touching a GPU); the two shards of the configs[3]
+    64 GiB stream tile it exactly; a WORLD_SIZE that contradicts --gpus exits 2."""
+    import json
+    import subprocess
+    import sys
+
+    from tests.oracle_util import ROOT
+
+    env = dict(os.environ, T3DES_BENCH_LAUNCH_PROBE="1")
+    env.pop("WORLD_SIZE", None)
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2"], capture_output=True,
+                       text=True, env=env, timeout=300)
+    assert p.returncode == 0, p.stderr[-2000:]
+    recs = sorted((json.loads(l) for l in p.stdout.splitlines() if l.startswith("{")), key=lambda r: r["rank"])
+    assert [r["rank"] for r in recs] == [0, 1] and all(r["world"] == 2 for r in recs)
+    n = (64 << 30) // 8
+    (f0, c0), (f1, c1) = recs[0]["shard"], recs[1]["shard"]
+    assert f0 == 0 and f1 == c0 and f1 + c1 == n
+    bad = dict(env, WORLD_SIZE="3")
+    assert subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2"], env=bad,
+                          capture_output=True, timeout=120).returncode == 2
