@@ -21,7 +21,6 @@ torch.cuda.init()
 GiB = 1 << 30
 buf = np.ones(GiB, dtype=np.uint8)  # faulted in
 base = buf.ctypes.data
-print(json.dumps({"pageable_access": torch.cuda.get_device_properties(0).__dict__.get("pageable_memory_access", "n/a")}))
 try:
     from cuda.bindings import runtime as rt  # cuda-python
     for a in ("cudaDevAttrPageableMemoryAccess", "cudaDevAttrPageableMemoryAccessUsesHostPageTables",
