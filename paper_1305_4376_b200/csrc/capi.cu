@@ -374,8 +374,10 @@ int ecb_host_staged(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8
         // threads with 4 MiB stages are best (26 GB/s end to end vs 7 GB/s
         // through the driver's own pageable copies)
         if (total <= 0) total = std::clamp(int(std::thread::hardware_concurrency()) * 3 / 4, 2, 12);
-        c->pool_in = new t3b::CopyPool((total + 1) / 2, node);
-        c->pool_out = new t3b::CopyPool(std::max(1, total / 2), node);
+        // experiments: streaming stores per direction (into the slots / out to the caller)
+        auto flag = [](const char* n, bool d) { const char* e = std::getenv(n); return e ? std::atoi(e) != 0 : d; };
+        c->pool_in = new t3b::CopyPool((total + 1) / 2, node, flag("T3DES_HOST_NT_IN", true));
+        c->pool_out = new t3b::CopyPool(std::max(1, total / 2), node, flag("T3DES_HOST_NT_OUT", true));
     }
     const std::size_t nst = (len + S - 1) / S;
     // One small stage between two pageable spans: copy in, run the SP-table

@@ -25,13 +25,9 @@ namespace {
 // memcpy with non-temporal (streaming) stores: the staged bytes are not read
 // again by this thread, and skipping the read-for-ownership of each
 // destination line saves a quarter of the host memory traffic of a copy.
-void stream_copy(char* d, const char* s, std::size_t n) {
+void stream_copy(char* d, const char* s, std::size_t n, bool nt) {
 #if defined(__x86_64__)
-    static const bool enabled = [] {
-        const char* e = std::getenv("T3DES_HOST_NT_COPY");
-        return !e || std::atoi(e) != 0;
-    }();
-    if (enabled && n >= 4096) {
+    if (nt && n >= 4096) {
         const std::size_t head = (16 - (reinterpret_cast<std::uintptr_t>(d) & 15)) & 15;
         std::memcpy(d, s, head);
         d += head;
@@ -53,7 +49,13 @@ void stream_copy(char* d, const char* s, std::size_t n) {
         return;
     }
 #endif
+    (void)nt;
     std::memcpy(d, s, n);
+}
+
+bool env_flag(const char* name, bool dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) != 0 : dflt;
 }
 
 constexpr int kMpolDefault = 0, kMpolPreferred = 1, kMpolBind = 2;  // linux/mempolicy.h
@@ -194,7 +196,8 @@ void host_free_on_node(void* p, std::size_t bytes, bool registered) {
     }
 }
 
-CopyPool::CopyPool(int nthreads, NumaNode node) : n_(std::max(1, nthreads)), node_(std::move(node)) {
+CopyPool::CopyPool(int nthreads, NumaNode node, bool streaming)
+    : n_(std::max(1, nthreads)), node_(std::move(node)), nt_(streaming && env_flag("T3DES_HOST_NT_COPY", true)) {
     th_.reserve(n_);
     for (int i = 0; i < n_; ++i) th_.emplace_back([this, i] { run(i); });
 }
@@ -250,7 +253,7 @@ void CopyPool::run(int i) {
         // piece i of n_, page-aligned so that threads never share a page
         const std::size_t per = ((b + n_ - 1) / n_ + 4095) & ~std::size_t(4095);
         const std::size_t lo = std::min(b, per * std::size_t(i)), hi = std::min(b, lo + per);
-        if (hi > lo) stream_copy(d + lo, s + lo, hi - lo);
+        if (hi > lo) stream_copy(d + lo, s + lo, hi - lo, nt_);
         {
             std::lock_guard<std::mutex> l(m_);
             if (--left_ == 0) done_cv_.notify_all();

@@ -63,8 +63,9 @@ void host_free_on_node(void* p, std::size_t bytes, bool registered);
 // start() hands out a job and returns; wait() blocks until it is done.
 class CopyPool {
 public:
-    // threads are bound to `node`'s CPUs when it is known
-    explicit CopyPool(int nthreads, NumaNode node = {});
+    // threads are bound to `node`'s CPUs when it is known; `streaming`: copy
+    // with non-temporal stores (the destination is not read again soon)
+    explicit CopyPool(int nthreads, NumaNode node = {}, bool streaming = true);
     ~CopyPool();
     CopyPool(const CopyPool&) = delete;
     CopyPool& operator=(const CopyPool&) = delete;
@@ -78,6 +79,7 @@ private:
     void run(int i);
     const int n_;
     const NumaNode node_;
+    const bool nt_;
     std::mutex m_;
     std::condition_variable cv_, done_cv_;
     std::uint64_t gen_ = 0;
