@@ -26,6 +26,8 @@ for c in CONFIGS:
     os.environ.update(T3DES_HOST_NT_IN=str(nt_in), T3DES_HOST_NT_OUT=str(nt_out), T3DES_HOST_COPY_THREADS=str(th))
     e = t3.Engine(0)
     e.set_schedule(ts)
+    os.environ["T3DES_HOST_STAGE_MIB"] = str(stage)
+    e.ecb_host(0, x.ctypes.data, y.ctypes.data, 64 << 20)  # creates the copy pools with this config's env
     engines[c] = e
 
 
