@@ -28,6 +28,8 @@ constexpr std::uint64_t kSpMinThreads = 128;  // SP-table CTA size floor for sma
 constexpr std::size_t kZeroCopyMaxBytes = std::size_t(64) << 20;  // scripts/zerocopy_{sweep,big}.py
 // pageable batches up to this size run their stages zero-copy on the pinned slots
 constexpr std::size_t kStagedZeroCopyMaxBytes = std::size_t(12) << 20;
+// host copy threads of the pageable staging path (in + out pools)
+constexpr int kMaxCopyThreads = 14;
 // SP-table launches that may use PDL (scripts/pdl_ab.py: 8-128 KiB enc+dec
 // chains 12.3 -> 7.7 us per pair; from 256 KiB the early CTAs cost more)
 constexpr std::uint64_t kPdlMaxBlocks = 16384;
@@ -370,13 +372,19 @@ int ecb_host_staged(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8
     if (!c->pool_in) {
         int total = c->copy_threads;
         if (const char* e = std::getenv("T3DES_HOST_COPY_THREADS")) total = std::atoi(e);
-        // measured on the 16-thread B200 hosts (scripts/gpu_pageable.sh): 12
-        // threads with 4 MiB stages are best (26 GB/s end to end vs 7 GB/s
-        // through the driver's own pageable copies)
-        if (total <= 0) total = std::clamp(int(std::thread::hardware_concurrency()) * 3 / 4, 2, 12);
-        // experiments: streaming stores per direction (into the slots / out to the caller)
+        // measured on the 16-thread B200 hosts (scripts/pageable_ab.py,
+        // profiles/r2/pageable_ab_r2k*.txt): 14 threads with 6 MiB stages and
+        // cached stores into the slots are best
+        if (total <= 0) total = std::clamp(int(std::thread::hardware_concurrency()) * 7 / 8, 2, kMaxCopyThreads);
+        // Copies into the pinned slots use ordinary (cached) stores: the slot
+        // stays in the CPU's last-level cache, where the H2D DMA reads it
+        // (DDIO) instead of from DRAM — +8-17% end to end over streaming
+        // stores (profiles/r2/pageable_ab_r2k*.txt).  Copies out to the
+        // caller's buffer use streaming stores (no read-for-ownership; the
+        // caller's data is not re-read by this thread).  Overrides for
+        // experiments: T3DES_HOST_NT_IN / T3DES_HOST_NT_OUT.
         auto flag = [](const char* n, bool d) { const char* e = std::getenv(n); return e ? std::atoi(e) != 0 : d; };
-        c->pool_in = new t3b::CopyPool((total + 1) / 2, node, flag("T3DES_HOST_NT_IN", true));
+        c->pool_in = new t3b::CopyPool((total + 1) / 2, node, flag("T3DES_HOST_NT_IN", false));
         c->pool_out = new t3b::CopyPool(std::max(1, total / 2), node, flag("T3DES_HOST_NT_OUT", true));
     }
     const std::size_t nst = (len + S - 1) / S;
@@ -837,7 +845,7 @@ int t3des_cu_ecb_multi(const int* devices, int ndev, const std::uint64_t sub48[4
             int same = 0;
             for (auto* o : ctx) same += o->numa.node == c->numa.node;
             const int cpus = c->numa.node >= 0 ? int(c->numa.cpus.size()) : hw;
-            c->copy_threads = std::clamp(cpus / std::max(same, 1), 2, 12);
+            c->copy_threads = std::clamp(cpus / std::max(same, 1), 2, kMaxCopyThreads);
         }
         workers.emplace_back([&, g, c] {
             std::uint64_t b0 = 0, cnt = 0;
@@ -876,7 +884,7 @@ int t3des_cu_ecb_workers(unsigned workers, int first_device, const std::uint64_t
         int rc = pool_acquire(first_device, &c);
         if (!rc && !c->pool_in) {
             c->numa_bind = true;
-            if (c->numa.node >= 0) c->copy_threads = std::clamp(int(c->numa.cpus.size()) * 3 / 4, 2, 12);
+            if (c->numa.node >= 0) c->copy_threads = std::clamp(int(c->numa.cpus.size()) * 7 / 8, 2, kMaxCopyThreads);
         }
         if (!rc) rc = t3des_cu_set_schedule(c, sub48);
         if (!rc) rc = t3des_cu_ecb_host(c, dir, in, out, len);

@@ -54,7 +54,7 @@ struct t3des_cu_ctx {
     bool hbuf_registered[kHostSlots] = {};  // allocated by host_alloc_on_node (mmap + register)
     t3b::CopyPool* pool_in = nullptr;
     t3b::CopyPool* pool_out = nullptr;
-    std::size_t stage_bytes = std::size_t(4) << 20;  // pageable stage size
+    std::size_t stage_bytes = std::size_t(6) << 20;  // pageable stage size (scripts/pageable_ab.py)
     int copy_threads = 0;                            // total host copy threads (0 = auto)
     t3b::NumaNode numa;      // the device's NUMA node (node -1: unknown / single-node host)
     bool numa_bind = false;  // place pinned staging and copy threads on `numa` (multi-GPU contexts)
