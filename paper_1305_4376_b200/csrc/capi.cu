@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <condition_variable>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -335,7 +336,7 @@ SpanKind classify_span(const void* p) {
 // (in or out) skips its host copy and DMAs straight from/to the span.
 int ecb_host_staged(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8_t* out, std::size_t len,
                     bool in_pinned, bool out_pinned) {
-    constexpr int R = t3des_cu_ctx::kHostSlots;
+    const int R = c->host_slots;
     std::size_t S = c->pipe_explicit ? c->pipe_chunk : c->stage_bytes;  // t3des_cu_set_pipeline
     if (!c->pipe_explicit && small_batch_stage(len)) S = small_batch_stage(len);
     if (const char* e = std::getenv("T3DES_HOST_STAGE_MIB")) S = std::size_t(std::max(1, std::atoi(e))) << 20;
@@ -344,7 +345,7 @@ int ecb_host_staged(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8
     const t3b::NumaNode none;
     const t3b::NumaNode& node = c->numa_bind ? c->numa : none;
     if (c->hbuf_bytes < S) {
-        for (int i = 0; i < R; ++i) {
+        for (int i = 0; i < t3des_cu_ctx::kHostSlots; ++i) {
             if (c->hev_live[i]) T3_CK(cudaEventSynchronize(c->hev[i]));
             t3b::host_free_on_node(c->hbuf[i], c->hbuf_bytes, c->hbuf_registered[i]);
             if (c->hdev[i]) cudaFree(c->hdev[i]);
@@ -417,49 +418,83 @@ int ecb_host_staged(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8
     if (const char* e = std::getenv("T3DES_ZEROCOPY_MAX")) zc_max = std::strtoull(e, nullptr, 10);  // experiments
     const bool zc = !in_pinned && !out_pinned && len <= zc_max && !c->chunk_blocks &&
                     (c->variant == T3DES_CU_VARIANT_AUTO || c->variant == T3DES_CU_VARIANT_SPTABLE);
-    // Errors never return with a copy job in flight (the pools would keep
-    // writing into the caller's buffers): every started job is waited for.
-    int rc = T3DES_CU_OK;
-    auto ck = [&](cudaError_t e) {
-        if (e != cudaSuccess && !rc) rc = T3DES_CU_ERR_CUDA;
-        return rc == T3DES_CU_OK;
-    };
-    for (std::size_t k = 0; k < nst + (R - 1) && !rc; ++k) {
-        const bool stage_in = k < nst;
-        const bool stage_out = k >= std::size_t(R - 1) && !out_pinned;
-        const std::size_t j = k - (R - 1);
-        const int slot = int(k % R);
-        bool in_started = false, out_started = false;
-        if (stage_in && !in_pinned && (!c->hev_live[slot] || ck(cudaEventSynchronize(c->hev[slot])))) {
-            c->pool_in->start(c->hbuf[slot], in + off(k), cnt(k));  // the slot's last D2H is done
-            in_started = true;
-        }
-        if (stage_out && ck(cudaEventSynchronize(c->hev[j % R]))) {
-            c->pool_out->start(out + off(j), c->hbuf[j % R], cnt(j));
-            out_started = true;
-        }
-        if (in_started) c->pool_in->wait();
-        if (stage_in && !rc) {
-            cudaStream_t s = c->st[slot];
-            const std::uint8_t* src = in_pinned ? in + off(k) : c->hbuf[slot];
-            std::uint8_t* dst = out_pinned ? out + off(k) : c->hbuf[slot];
-            const std::size_t n = cnt(k);
-            if (zc) {  // the SP-table kernel on the mapped pinned slot
-                void* d = nullptr;
-                if (cudaHostGetDevicePointer(&d, c->hbuf[slot], 0) != cudaSuccess) rc = T3DES_CU_ERR_CUDA;
-                if (!rc) rc = launch_sptable(c, dir, static_cast<std::uint8_t*>(d), static_cast<std::uint8_t*>(d), n / 8, s);
-            } else {
-                if (cudaMemcpyAsync(c->hdev[slot], src, n, cudaMemcpyHostToDevice, s) != cudaSuccess) rc = T3DES_CU_ERR_CUDA;
-                if (!rc) rc = run_device(c, dir, c->hdev[slot], c->hdev[slot], n / 8, s);
-                if (!rc && cudaMemcpyAsync(dst, c->hdev[slot], n, cudaMemcpyDeviceToHost, s) != cudaSuccess)
-                    rc = T3DES_CU_ERR_CUDA;
+    // Fill side (this thread) and drain side (c->drain) run decoupled over the
+    // ring of R slots: the fill side copies stage k into slot k % R once the
+    // drain side has released it, then enqueues H2D -> kernel -> D2H (or the
+    // zero-copy kernel) and an event; the drain side waits for stage j's
+    // event, copies it out of its slot and releases the slot.  Neither side
+    // waits for the other's copy to finish unless the ring is full or empty
+    // (the lock-step loop of round 1 ran both copies per step and waited for
+    // the slower one).  Errors never return with a copy job in flight: each
+    // side waits for its own copies, and the drain side is joined.
+    std::mutex mu;
+    std::condition_variable cv;
+    std::size_t enqueued = 0, released = 0;
+    int rc = T3DES_CU_OK, drain_rc = T3DES_CU_OK;
+    bool stop = false;
+    if (!c->drain) c->drain = new t3b::Worker();
+    c->drain->run([&] {
+        for (std::size_t j = 0; j < nst; ++j) {
+            {
+                std::unique_lock<std::mutex> l(mu);
+                cv.wait(l, [&] { return stop || enqueued > j; });
+                if (enqueued <= j) return;  // the fill side stopped early
             }
-            if (!rc && cudaEventRecord(c->hev[slot], s) != cudaSuccess) rc = T3DES_CU_ERR_CUDA;
-            c->hev_live[slot] = !rc;
+            int r = cudaEventSynchronize(c->hev[j % R]) == cudaSuccess ? T3DES_CU_OK : T3DES_CU_ERR_CUDA;
+            if (!r && !out_pinned) {
+                c->pool_out->start(out + off(j), c->hbuf[j % R], cnt(j));
+                c->pool_out->wait();
+            }
+            std::lock_guard<std::mutex> l(mu);
+            if (r) {
+                drain_rc = r;
+                stop = true;
+                cv.notify_all();
+                return;
+            }
+            released = j + 1;
+            cv.notify_all();
         }
-        if (out_started) c->pool_out->wait();
+    });
+    for (std::size_t k = 0; k < nst && !rc; ++k) {
+        const int slot = int(k % R);
+        {
+            std::unique_lock<std::mutex> l(mu);
+            cv.wait(l, [&] { return stop || k < std::size_t(R) || released + R > k; });
+            if (stop) break;
+        }
+        if (!in_pinned) {  // the slot's last stage has been copied out (or DMA'd to a pinned out)
+            c->pool_in->start(c->hbuf[slot], in + off(k), cnt(k));
+            c->pool_in->wait();
+        }
+        cudaStream_t s = c->st[slot];
+        const std::uint8_t* src = in_pinned ? in + off(k) : c->hbuf[slot];
+        std::uint8_t* dst = out_pinned ? out + off(k) : c->hbuf[slot];
+        const std::size_t n = cnt(k);
+        if (zc) {  // the SP-table kernel on the mapped pinned slot
+            void* d = nullptr;
+            if (cudaHostGetDevicePointer(&d, c->hbuf[slot], 0) != cudaSuccess) rc = T3DES_CU_ERR_CUDA;
+            if (!rc) rc = launch_sptable(c, dir, static_cast<std::uint8_t*>(d), static_cast<std::uint8_t*>(d), n / 8, s);
+        } else {
+            if (cudaMemcpyAsync(c->hdev[slot], src, n, cudaMemcpyHostToDevice, s) != cudaSuccess) rc = T3DES_CU_ERR_CUDA;
+            if (!rc) rc = run_device(c, dir, c->hdev[slot], c->hdev[slot], n / 8, s);
+            if (!rc && cudaMemcpyAsync(dst, c->hdev[slot], n, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+                rc = T3DES_CU_ERR_CUDA;
+        }
+        if (!rc && cudaEventRecord(c->hev[slot], s) != cudaSuccess) rc = T3DES_CU_ERR_CUDA;
+        c->hev_live[slot] = !rc;
+        std::lock_guard<std::mutex> l(mu);
+        if (rc) {
+            stop = true;
+        } else {
+            enqueued = k + 1;
+        }
+        cv.notify_all();
     }
-    for (int i = 0; i < R; ++i) ck(cudaStreamSynchronize(c->st[i]));
+    c->drain->wait();
+    if (!rc) rc = drain_rc;
+    for (int i = 0; i < R; ++i)
+        if (cudaStreamSynchronize(c->st[i]) != cudaSuccess && !rc) rc = T3DES_CU_ERR_CUDA;
     if (rc) (void)cudaGetLastError();
     return rc;
 }
@@ -534,6 +569,8 @@ int t3des_cu_create(int device, t3des_cu_ctx** out) {
         char bus[32] = {};
         if (cudaDeviceGetPCIBusId(bus, sizeof bus, device) == cudaSuccess) c->numa = t3b::numa_node_of_pci(bus);
         (void)cudaGetLastError();
+        if (const char* e = std::getenv("T3DES_HOST_SLOTS"))  // experiments: pageable ring depth
+            c->host_slots = std::clamp(std::atoi(e), 2, t3des_cu_ctx::kHostSlots);
         // T3DES_NUMA=1: place single-device contexts too (multi-GPU contexts always are)
         if (const char* e = std::getenv("T3DES_NUMA")) c->numa_bind = std::atoi(e) == 1;
     }
@@ -622,6 +659,7 @@ int t3des_cu_destroy(t3des_cu_ctx* c) {
         }
         delete c->pool_in;
         delete c->pool_out;
+        delete c->drain;
         if (c->d_sp) cudaFree(c->d_sp);
         if (c->d_acc) cudaFree(c->d_acc);
         (void)cudaGetLastError();

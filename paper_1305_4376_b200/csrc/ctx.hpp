@@ -45,7 +45,7 @@ struct t3des_cu_ctx {
     bool pipe_explicit = false;  // set by t3des_cu_set_pipeline; else stages adapt to the batch
     // pageable-span staging (t3des_cu_ecb_host): pinned ring, one event per
     // slot (the slot's last GPU use), and two host copy pools (in / out)
-    static constexpr int kHostSlots = 4;
+    static constexpr int kHostSlots = 8;  // ring capacity; host_slots of them are used
     std::uint8_t* hbuf[kHostSlots] = {};
     std::uint8_t* hdev[kHostSlots] = {};
     std::size_t hbuf_bytes = 0;
@@ -54,6 +54,8 @@ struct t3des_cu_ctx {
     bool hbuf_registered[kHostSlots] = {};  // allocated by host_alloc_on_node (mmap + register)
     t3b::CopyPool* pool_in = nullptr;
     t3b::CopyPool* pool_out = nullptr;
+    t3b::Worker* drain = nullptr;  // drain side of the pageable ring (copies out)
+    int host_slots = 4;            // pinned ring slots in use (<= kHostSlots)
     std::size_t stage_bytes = std::size_t(6) << 20;  // pageable stage size (scripts/pageable_ab.py)
     int copy_threads = 0;                            // total host copy threads (0 = auto)
     t3b::NumaNode numa;      // the device's NUMA node (node -1: unknown / single-node host)

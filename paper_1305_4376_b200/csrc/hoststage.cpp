@@ -261,4 +261,44 @@ void CopyPool::run(int i) {
     }
 }
 
+Worker::Worker() {
+    th_ = std::thread([this] {
+        std::unique_lock<std::mutex> l(m_);
+        for (;;) {
+            cv_.wait(l, [&] { return stop_ || static_cast<bool>(job_); });
+            if (stop_) return;
+            auto job = std::move(job_);
+            job_ = nullptr;
+            l.unlock();
+            job();
+            l.lock();
+            busy_ = false;
+            done_cv_.notify_all();
+        }
+    });
+}
+
+Worker::~Worker() {
+    {
+        std::lock_guard<std::mutex> l(m_);
+        stop_ = true;
+    }
+    cv_.notify_all();
+    th_.join();
+}
+
+void Worker::run(std::function<void()> job) {
+    {
+        std::lock_guard<std::mutex> l(m_);
+        job_ = std::move(job);
+        busy_ = true;
+    }
+    cv_.notify_all();
+}
+
+void Worker::wait() {
+    std::unique_lock<std::mutex> l(m_);
+    done_cv_.wait(l, [&] { return !busy_; });
+}
+
 }  // namespace t3b

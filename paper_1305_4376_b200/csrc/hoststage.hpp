@@ -11,6 +11,7 @@
 #include <condition_variable>
 #include <cstddef>
 #include <cstdint>
+#include <functional>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -89,6 +90,27 @@ private:
     const char* src_ = nullptr;
     std::size_t bytes_ = 0;
     std::vector<std::thread> th_;
+};
+
+// One persistent thread that runs one job at a time: run() hands it a job
+// and returns; wait() blocks until the job has finished.  The pageable
+// staging path's drain side (copies out of the ring) runs on it, decoupled
+// from the fill side on the calling thread.
+class Worker {
+public:
+    Worker();
+    ~Worker();
+    Worker(const Worker&) = delete;
+    Worker& operator=(const Worker&) = delete;
+    void run(std::function<void()> job);
+    void wait();
+
+private:
+    std::mutex m_;
+    std::condition_variable cv_, done_cv_;
+    std::function<void()> job_;
+    bool busy_ = false, stop_ = false;
+    std::thread th_;
 };
 
 }  // namespace t3b
