@@ -58,7 +58,7 @@ bool env_flag(const char* name, bool dflt) {
     return e ? std::atoi(e) != 0 : dflt;
 }
 
-constexpr int kMpolDefault = 0, kMpolPreferred = 1, kMpolBind = 2;  // linux/mempolicy.h
+constexpr int kMpolDefault = 0, kMpolPreferred = 1;  // linux/mempolicy.h
 constexpr unsigned long kMaxNode = 1024;                            // bits in the masks below
 
 std::string sysfs_root() {
@@ -173,7 +173,8 @@ int host_alloc_on_node(std::size_t bytes, const NumaNode& n, void** out, bool* r
     if (p == MAP_FAILED) return int(cudaErrorMemoryAllocation);
     unsigned long mask[kMaxNode / (8 * sizeof(unsigned long))] = {};
     mask[n.node / (8 * sizeof(unsigned long))] |= 1ul << (n.node % (8 * sizeof(unsigned long)));
-    (void)syscall(SYS_mbind, p, bytes, kMpolBind, mask, kMaxNode, 0u);  // best effort: placement, not correctness
+    // preferred, not bound: a full node falls back to another instead of failing
+    (void)syscall(SYS_mbind, p, bytes, kMpolPreferred, mask, kMaxNode, 0u);
     std::memset(p, 0, bytes);                                         // fault the pages in on that node
     const cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
     if (e != cudaSuccess) {

@@ -53,8 +53,8 @@ private:
     unsigned char old_cpus_[128] = {};  // cpu_set_t storage
 };
 
-// Page-locked host memory on a NUMA node: mmap + mbind(MPOL_BIND) + first
-// touch + cudaHostRegister (mapped, portable), so the pages are where the
+// Page-locked host memory on a NUMA node: mmap + mbind(MPOL_PREFERRED) +
+// first touch + cudaHostRegister (mapped, portable), so the pages are where the
 // device's DMA and copy threads are.  node < 0 falls back to cudaMallocHost.
 // Returns 0 or a cudaError_t value.
 int host_alloc_on_node(std::size_t bytes, const NumaNode& n, void** out, bool* registered);
