@@ -152,13 +152,23 @@ int t3des_cu_ecb_workers(unsigned workers, int first_device, const uint64_t sub4
  * live on `home_device`; shard g (t3des_cu_shard_range) is copied to
  * devices[g] with cudaMemcpyPeerAsync, transformed there and copied back.
  * A shard whose device is the home device is transformed in place of
- * din -> dout without copies unless flags & T3DES_CU_MULTI_STAGE_ALL.
+ * din -> dout without copies unless flags & T3DES_CU_MULTI_STAGE_ALL; the
+ * shard sizes are t3des_cu_multi_device_shards (the home shard weighted).
  * Each staged shard is pipelined in chunks over three streams of its device
  * (peer copy in, kernel, peer copy out overlap chunk by chunk).
  * Synchronous.  Peer access is enabled where the topology allows it. */
 #define T3DES_CU_MULTI_STAGE_ALL 1
 int t3des_cu_ecb_multi_device(const int* devices, int ndev, const uint64_t sub48[48], int direction,
                               int home_device, const void* din, void* dout, size_t len, int flags);
+
+/* The block ranges t3des_cu_ecb_multi_device gives each of its `ndev`
+ * devices for a payload resident on `home` (first[g], count[g]): the home
+ * GPU's shard, which needs no NVLink copy, is weighted against the remote
+ * shards' peer-copy bound (about a third of the blocks at 3+ GPUs); equal
+ * tile-rounded ranges when the home GPU is not among the devices exactly once
+ * or with T3DES_CU_MULTI_STAGE_ALL. */
+int t3des_cu_multi_device_shards(const int* devices, int ndev, int home, uint64_t nblocks, int flags,
+                                 uint64_t* first, uint64_t* count);
 
 /* The block range device `g` of `ndev` owns in t3des_cu_ecb_multi (and in
  * bench.py's torchrun ranks): [first, first + count), boundaries at

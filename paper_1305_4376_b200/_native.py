@@ -67,6 +67,7 @@ SIGNATURES = {
     "t3des_cu_ecb_multi": (_i, [ctypes.POINTER(_i), _i, _u64p, _i, _vp, _vp, _sz]),
     "t3des_cu_ecb_workers": (_i, [ctypes.c_uint, _i, _u64p, _i, _vp, _vp, _sz]),
     "t3des_cu_ecb_multi_device": (_i, [ctypes.POINTER(_i), _i, _u64p, _i, _i, _vp, _vp, _sz, _i]),
+    "t3des_cu_multi_device_shards": (_i, [ctypes.POINTER(_i), _i, _i, ctypes.c_uint64, _i, _u64p, _u64p]),
     "t3des_cu_shard_range": (_i, [ctypes.c_uint64, _i, _i, _u64p, _u64p]),
     "t3des_cu_host_alloc": (_i, [_sz, ctypes.POINTER(_vp)]),
     "t3des_cu_host_free": (_i, [_vp]),

@@ -282,6 +282,50 @@ std::size_t small_batch_stage(std::size_t len) {
     return std::max<std::size_t>(s, 8);
 }
 
+// Block-range cuts of t3des_cu_ecb_multi_device.  With the payload resident
+// on `home`, every remote shard crosses the home GPU's NVLink ports twice
+// (peer copy out and back), while the home GPU's own shard needs no copy.  So
+// the home shard gets the share h that balances its kernel time against the
+// remote side's bound: h / r_k = (1 - h) / min(r_link, (n_remote) * r_k), with
+// r_k = 396 GB/s (the kernel, bench) and r_link = 770 GB/s per direction (the
+// measured B200 peer-copy rate, B200_PROFILING.md) — h = 0.34 for 3+ GPUs, 0.5
+// for 2.  Equal shards (t3des_cu_shard_range) when the home GPU is
+// not among the devices exactly once, or with T3DES_CU_MULTI_STAGE_ALL.
+// T3DES_MULTI_HOME_SHARE overrides h (tests, tuning).  Cuts are whole tiles.
+std::vector<std::uint64_t> multi_device_cuts(const int* devices, int ndev, int home, std::uint64_t nblocks,
+                                             int flags) {
+    std::vector<std::uint64_t> cut(ndev + 1, nblocks);
+    int home_idx = -1, homes = 0;
+    for (int g = 0; g < ndev; ++g)
+        if (devices[g] == home) {
+            if (home_idx < 0) home_idx = g;
+            ++homes;
+        }
+    double h = -1.0;
+    if (const char* e = std::getenv("T3DES_MULTI_HOME_SHARE")) h = std::atof(e);
+    else if (homes == 1 && ndev > 1 && !(flags & T3DES_CU_MULTI_STAGE_ALL)) {
+        constexpr double kKernelGBps = 396.0, kLinkGBps = 770.0;
+        h = kKernelGBps / (kKernelGBps + std::min(kLinkGBps, (ndev - 1) * kKernelGBps));
+    }
+    if (home_idx < 0 || ndev == 1 || !(h > 0.0 && h < 1.0)) {
+        for (int g = 0; g < ndev; ++g) {
+            std::uint64_t f = 0, c = 0;
+            t3des_cu_shard_range(nblocks, ndev, g, &f, &c);
+            cut[g] = f;
+        }
+        return cut;
+    }
+    const double rest = (1.0 - h) / (ndev - 1);
+    double acc = 0.0;
+    for (int g = 0; g < ndev; ++g) {
+        const std::uint64_t b = std::uint64_t(acc * double(nblocks));
+        cut[g] = g == 0 ? 0 : std::min(nblocks, b - b % T3_TILE_BLOCKS);
+        acc += g == home_idx ? h : rest;
+    }
+    for (int g = 1; g <= ndev; ++g) cut[g] = std::max(cut[g], cut[g - 1]);  // monotone
+    return cut;
+}
+
 }  // namespace
 
 namespace t3b {
@@ -956,9 +1000,9 @@ int t3des_cu_ecb_multi_device(const int* devices, int ndev, const std::uint64_t 
     constexpr std::uint64_t kTileBytes = 8 * T3_TILE_BLOCKS;
     std::uint64_t chunk_override = 0;
     if (const char* e = std::getenv("T3DES_MULTI_CHUNK_BYTES")) chunk_override = std::strtoull(e, nullptr, 10);
+    const std::vector<std::uint64_t> cut = multi_device_cuts(devices, ndev, home, nblocks, flags);
     for (int g = 0; g < ndev && !rc; ++g) {
-        std::uint64_t first = 0, count = 0;
-        t3des_cu_shard_range(nblocks, ndev, g, &first, &count);
+        const std::uint64_t first = cut[g], count = cut[g + 1] - cut[g];
         if (!count) continue;
         rc = pool_acquire(devices[g], &ctx[g]);
         if (!rc) rc = t3des_cu_set_schedule(ctx[g], sub48);
@@ -1006,6 +1050,17 @@ int t3des_cu_ecb_multi_device(const int* devices, int ndev, const std::uint64_t 
     }
     (void)cudaGetLastError();
     return rc;
+}
+
+int t3des_cu_multi_device_shards(const int* devices, int ndev, int home, std::uint64_t nblocks, int flags,
+                                 std::uint64_t* first, std::uint64_t* count) {
+    if (!devices || ndev <= 0 || !first || !count) return T3DES_CU_ERR_ARG;
+    const std::vector<std::uint64_t> cut = multi_device_cuts(devices, ndev, home, nblocks, flags);
+    for (int g = 0; g < ndev; ++g) {
+        first[g] = cut[g];
+        count[g] = cut[g + 1] - cut[g];
+    }
+    return T3DES_CU_OK;
 }
 
 int t3des_cu_host_alloc(std::size_t bytes, void** out) {

@@ -474,6 +474,24 @@ def test_multi_device_resident_scatter_gather(oracle):
     assert rc == 0 and np.array_equal(b[5: 5 + x.nbytes].cpu().numpy(), oracle.ecb(x, s, 0))
 
 
+@pytest.mark.parametrize("home_share", [None, "0.2", "0.5"])
+def test_multi_device_weighted_home_shard(oracle, monkeypatch, home_share):
+    """ecb_multi_device with a weighted home shard (T3DES_MULTI_HOME_SHARE
+    forces the weighting on this one-GPU box, devices [0, 0, 0]): the home
+    shard runs in place, the others staged; bytes equal the oracle."""
+    if home_share:
+        monkeypatch.setenv("T3DES_MULTI_HOME_SHARE", home_share)
+    devs = [0, 0, 0]
+    s = oracle.schedule_hex(KEYS[0])
+    n = 1024 * 37 + 11
+    x = oracle.splitmix(7, n, 0xD0E)
+    src = dev(x)
+    dst = torch.empty_like(src)
+    arr = (ctypes.c_int * 3)(*devs)
+    assert N.lib().t3des_cu_ecb_multi_device(arr, 3, s, 0, 0, src.data_ptr(), dst.data_ptr(), x.nbytes, 0) == 0
+    assert np.array_equal(host(dst), oracle.ecb(x, s, 0))
+
+
 @pytest.mark.parametrize("chunk_bytes,n", [(8 * 1000 + 8, 3 * 1024 * 9 + 5), (None, (72 << 20) // 8 + 13)])
 def test_multi_device_chunk_pipeline(oracle, monkeypatch, chunk_bytes, n):
     """ecb_multi_device with STAGE_ALL: every shard runs as a chunk pipeline

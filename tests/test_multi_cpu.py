@@ -116,3 +116,40 @@ def test_bench_self_launches_n_ranks():
     bad = dict(env, WORLD_SIZE="3")
     assert subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2"], env=bad,
                           capture_output=True, timeout=120).returncode == 2
+
+
+def _md_shards(devs, home, n, flags=0):
+    import ctypes
+
+    from paper_1305_4376_b200 import _native as N
+
+    k = len(devs)
+    f, c = (ctypes.c_uint64 * k)(), (ctypes.c_uint64 * k)()
+    assert N.lib().t3des_cu_multi_device_shards((ctypes.c_int * k)(*devs), k, home, n, flags, f, c) == 0
+    return list(f), list(c)
+
+
+@pytest.mark.parametrize("n", [0, 1, 1023, 5 * TILE_BLOCKS + 17, (64 << 30) // 8])
+def test_multi_device_home_weighted_shards(n, monkeypatch):
+    """t3des_cu_ecb_multi_device's split for data resident on `home`: the home
+    shard (no NVLink copy) is weighted against the remote peer-copy bound —
+    h = 396 / (396 + min(770, (G-1) * 396)): 0.5 at G = 2, ~0.34 from G = 3 —
+    contiguous tile-aligned ranges covering [0, n); equal shards when the
+    home GPU is absent, duplicated, or with STAGE_ALL."""
+    monkeypatch.delenv("T3DES_MULTI_HOME_SHARE", raising=False)
+    for devs, home, want_h in (([0, 1, 2, 3, 4, 5, 6, 7], 0, 396 / (396 + 770)), ([0, 1], 0, 0.5),
+                               ([3, 1, 2], 1, 396 / (396 + 770))):
+        f, c = _md_shards(devs, home, n)
+        assert f[0] == 0 and sum(c) == n and all(f[g + 1] == f[g] + c[g] for g in range(len(devs) - 1))
+        assert all(x % TILE_BLOCKS == 0 for x in f)
+        hi = devs.index(home)
+        if n >= 64 * TILE_BLOCKS * len(devs):
+            assert abs(c[hi] / n - want_h) < 0.001
+            rest = [c[g] for g in range(len(devs)) if g != hi]
+            assert max(rest) - min(rest) <= 2 * TILE_BLOCKS
+    for devs, home, flags in (([1, 2, 3], 0, 0), ([0, 0, 0], 0, 0), ([0, 1, 2], 0, 1)):
+        f, c = _md_shards(devs, home, n, flags)
+        assert [(a, b) for a, b in zip(f, c)] == [shard_range(n, len(devs), g) for g in range(len(devs))]
+    monkeypatch.setenv("T3DES_MULTI_HOME_SHARE", "0.2")
+    f, c = _md_shards([0, 0, 0], 0, n)
+    assert sum(c) == n and (n < 64 * TILE_BLOCKS or abs(c[0] / n - 0.2) < 0.001)
