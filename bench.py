@@ -604,11 +604,21 @@ def main() -> None:
         else:
             dist.init_process_group(backend)
 
+    # host-side barrier (gloo): ranks that wait on it leave their GPUs idle,
+    # unlike an NCCL barrier, whose kernel spins on the GPU — which would
+    # time-slice with rank 0 driving every GPU in the e2e.multi leg
+    hostgroup = dist.new_group(backend="gloo") if world > 1 else None
+
     def barrier():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+
+    def host_barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier(group=hostgroup)
 
     def max_over_ranks(x: float) -> float:
         if world == 1:
@@ -841,8 +851,9 @@ def main() -> None:
             "path": "the pageable buffer registered once with t3des_cu_host_register (opt-in, outside the timing)"}
         del page
         # one process driving all N GPUs through t3des_cu_ecb_multi (the
-        # workers axis of DispatchConfig): rank 0, the other ranks idle
-        barrier()
+        # workers axis of DispatchConfig): rank 0, the other ranks idle on a
+        # host-side barrier
+        host_barrier()
         if rank == 0:
             devs = [r % max(ndev, 1) for r in range(world)]
             mh = torch.empty(world * one, dtype=torch.uint8).pin_memory()
@@ -861,7 +872,7 @@ def main() -> None:
                                     "path": "t3des_cu_ecb_multi from one process (one host thread + context per "
                                             "device, pinned buffer), the GPU reading of DispatchConfig.workers"}
             del mh
-        barrier()
+        host_barrier()
         del host
     else:
         line["e2e"] = None
@@ -876,7 +887,7 @@ def main() -> None:
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
-        dist.barrier()
+        host_barrier()
         dist.destroy_process_group()
     e.close()
 
