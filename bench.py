@@ -164,10 +164,17 @@ class CpuRef:
         self.s = self.o.schedule_hex(BENCH_KEY)
         self.kind = "reference" if self.o.ref is not None else "port"
 
+    @staticmethod
+    def all_threads() -> int:
+        # explicit, not the reference's workers = 0: that resolves through
+        # omp_get_max_threads(), which torchrun pins to 1 (OMP_NUM_THREADS=1)
+        try:
+            return len(os.sched_getaffinity(0))
+        except AttributeError:  # pragma: no cover
+            return os.cpu_count() or 1
+
     def threads(self, workers: int) -> int:
-        if self.o.ref is not None:
-            return int(self.o.ref.ref_resolve_workers(workers))
-        return workers or (os.cpu_count() or 1)
+        return workers or self.all_threads()
 
     def payload(self, nbytes: int):
         # the first nbytes of the bench's global payload (block i =
@@ -175,6 +182,7 @@ class CpuRef:
         return self.o.splitmix(0, nbytes // 8, SEED)
 
     def encrypt(self, buf, out, workers: int) -> float:
+        workers = self.threads(workers)
         t0 = time.perf_counter()
         if self.o.ref is not None:
             rc = self.o.ref.ref_ecb(buf.ctypes.data, out.ctypes.data, buf.nbytes, self.s, 0, 1, workers, 0, 0)
@@ -208,7 +216,7 @@ def cpu_reference_arm(full_bytes: int = 1 << 30, one_thread_bytes: int = 64 << 2
     return {
         "value": round(full_bytes / best / 1e9, 4), "unit": "GB/s", "cores": cores, "kind": r.kind,
         "sample": f"encrypt of the full {full_bytes >> 20} MiB configs[1] payload (the bench's splitmix stream, "
-                  f"bench key), {r.what()}, workers=0 -> {cores} threads, 1 warm-up + min of 3",
+                  f"bench key), {r.what()}, workers={cores} (all host threads), 1 warm-up + min of 3",
         "cpu_model": cpu_model(), "host_threads": os.cpu_count(),
         "workers_1": {"value": round(one_thread_bytes / best1 / 1e9, 4), "unit": "GB/s", "cores": 1,
                       "sample": f"first {one_thread_bytes >> 20} MiB of the same payload, workers=1, "
@@ -236,7 +244,7 @@ def run_reference_impl(args, rank: int, world: int) -> None:
     gbs = args.steps * nbytes / sum(times) / 1e9
     cores = r.threads(0)
     sample = (f"{'whole' if world == 1 else 'sample of the'} workload: encrypt of {nbytes >> 20} MiB (the first GiB "
-              f"of the bench's splitmix stream, bench key) per step, {r.what()}, workers=0 -> {cores} threads; "
+              f"of the bench's splitmix stream, bench key) per step, {r.what()}, workers={cores} (all host threads); "
               f"value = {args.steps} steps x {nbytes >> 20} MiB / their total time (best step "
               f"{nbytes / min(times) / 1e9:.4f} GB/s); cpu: {cpu_model()}")
     line = {
