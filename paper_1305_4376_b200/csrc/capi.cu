@@ -420,7 +420,7 @@ int ecb_host_staged(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8
         // measured on the 16-thread B200 hosts (scripts/pageable_ab.py,
         // profiles/r2/pageable_ab_r2k*.txt): 14 threads with 6 MiB stages and
         // cached stores into the slots are best
-        if (total <= 0) total = std::clamp(int(std::thread::hardware_concurrency()) * 7 / 8, 2, kMaxCopyThreads);
+        if (total <= 0) total = std::clamp(t3b::available_cpus() * 7 / 8, 2, kMaxCopyThreads);
         // Copies into the pinned slots use ordinary (cached) stores: the slot
         // stays in the CPU's last-level cache, where the H2D DMA reads it
         // (DDIO) instead of from DRAM — +8-17% end to end over streaming
@@ -917,7 +917,7 @@ int t3des_cu_ecb_multi(const int* devices, int ndev, const std::uint64_t sub48[4
         for (auto* c : ctx) pool_release(c, true);
         return rc;
     }
-    const int hw = std::max(1, int(std::thread::hardware_concurrency()));
+    const int hw = t3b::available_cpus();
     std::vector<int> rcs(ndev, T3DES_CU_OK);
     std::vector<std::thread> workers;
     for (int g = 0; g < ndev; ++g) {

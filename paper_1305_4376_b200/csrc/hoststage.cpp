@@ -90,6 +90,13 @@ int count_nodes(const std::string& root) {
 
 }  // namespace
 
+int available_cpus() {
+    cpu_set_t set;
+    CPU_ZERO(&set);
+    if (sched_getaffinity(0, sizeof set, &set) == 0) return std::max(1, CPU_COUNT(&set));
+    return std::max(1, int(std::thread::hardware_concurrency()));
+}
+
 std::vector<int> parse_cpulist(const char* s) {
     std::vector<int> cpus;
     if (!s) return cpus;

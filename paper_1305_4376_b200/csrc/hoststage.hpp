@@ -26,6 +26,10 @@ struct NumaNode {
     std::vector<int> cpus;  // the node's CPUs that this process may run on
 };
 
+// CPUs this process may run on (its affinity mask; e.g. a bench rank bound
+// to its GPU's node), at least 1.
+int available_cpus();
+
 // "0-3,8,10-11" -> {0,1,2,3,8,10,11}; malformed input -> {}.
 std::vector<int> parse_cpulist(const char* s);
 
