@@ -373,11 +373,11 @@ SpanKind classify_span(const void* p) {
 }
 
 // Pageable spans (hoststage.hpp): stage k goes through pinned slot k % R and
-// stream st[k % R].  Per iteration the in-pool copies stage k into its slot
-// while the out-pool copies stage k - (R - 1) out of its slot (after that
-// stage's D2H event), then stage k's H2D -> kernel -> D2H is enqueued, so up
-// to R - 1 stages are on the GPU while the host threads copy.  A pinned side
-// (in or out) skips its host copy and DMAs straight from/to the span.
+// stream st[k % R], R = c->host_slots.  A fill side (this thread, pool_in)
+// and a drain side (c->drain, pool_out) run decoupled — see the loop below —
+// so up to R - 1 stages are on the GPU while the host threads copy.  A
+// pinned side (in or out) skips its host copy and DMAs straight from/to the
+// span.
 int ecb_host_staged(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8_t* out, std::size_t len,
                     bool in_pinned, bool out_pinned) {
     const int R = c->host_slots;
