@@ -154,10 +154,14 @@ int t3des_cu_ecb_workers(unsigned workers, int first_device, const uint64_t sub4
  * A shard whose device is the home device is transformed in place of
  * din -> dout without copies unless flags & T3DES_CU_MULTI_STAGE_ALL; the
  * shard sizes are t3des_cu_multi_device_shards (the home shard weighted).
- * Each staged shard is pipelined in chunks over three streams of its device
- * (peer copy in, kernel, peer copy out overlap chunk by chunk).
+ * A remote shard whose device can map the home GPU's memory runs
+ * peer-direct: its kernel loads and stores the home buffers over NVLink, so
+ * transfer and compute overlap inside the kernel with no staging.  Otherwise
+ * (or with T3DES_CU_MULTI_COPY) it is pipelined in chunks over three streams
+ * of its device (peer copy in, kernel, peer copy out overlap chunk by chunk).
  * Synchronous.  Peer access is enabled where the topology allows it. */
-#define T3DES_CU_MULTI_STAGE_ALL 1
+#define T3DES_CU_MULTI_STAGE_ALL 1 /* every shard, the home one too, through the copy pipeline */
+#define T3DES_CU_MULTI_COPY 2      /* remote shards through the copy pipeline even with peer access */
 int t3des_cu_ecb_multi_device(const int* devices, int ndev, const uint64_t sub48[48], int direction,
                               int home_device, const void* din, void* dout, size_t len, int flags);
 

@@ -35,6 +35,8 @@ VARIANT_BITSLICE_DFMA = 4
 VARIANT_BITSLICE_SHRFMA = 5
 VARIANT_AUTO = 6
 AUTO_SMALL_BLOCKS = 131072
+MULTI_STAGE_ALL = 1  # t3des_cu_ecb_multi_device flags
+MULTI_COPY = 2
 
 class StreamReportC(ctypes.Structure):
     """t3des_cu_stream_report (include/t3des_cu.h)."""

@@ -991,8 +991,10 @@ int t3des_cu_ecb_multi_device(const int* devices, int ndev, const std::uint64_t 
     const bool aligned = ((reinterpret_cast<std::uintptr_t>(in) | reinterpret_cast<std::uintptr_t>(out)) & 7u) == 0;
     std::vector<t3des_cu_ctx*> ctx(ndev, nullptr);
     int rc = T3DES_CU_OK;
-    // Issue every shard asynchronously on its device, then wait.  A staged
-    // shard runs as a chunk pipeline over kStreams streams and staging
+    // Issue every shard asynchronously on its device, then wait.  A remote
+    // shard runs peer-direct where the devices can map each other's memory
+    // (below), else — or with T3DES_CU_MULTI_COPY — as a chunk pipeline
+    // over kStreams streams and staging
     // buffers of its context: chunk k = peer copy in -> kernel -> peer copy
     // out on stream k % kStreams, so chunk k's copy in overlaps chunk k-1's
     // kernel and chunk k-2's copy out (NVLink both directions + SMs busy).
@@ -1014,13 +1016,29 @@ int t3des_cu_ecb_multi_device(const int* devices, int ndev, const std::uint64_t 
             rc = run_device(c, dir, in + 8 * first, out + 8 * first, count, c->st[0]);
             continue;
         }
+        bool peer = false;
         if (devices[g] != home) {
             int can = 0;
             if (cudaDeviceCanAccessPeer(&can, devices[g], home) == cudaSuccess && can) {
                 const cudaError_t e = cudaDeviceEnablePeerAccess(home, 0);
                 if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) rc = T3DES_CU_ERR_CUDA;
                 (void)cudaGetLastError();
+                peer = !rc;
             }
+        }
+        // Peer-direct (NVLink 5 / NVSwitch): the shard's kernel runs on its
+        // device straight on the home GPU's buffers — loads and stores cross
+        // NVLink inside the kernel, so transfer and compute overlap tile by
+        // tile with no staging copies.  Plain 128-bit loads (the LDG variant):
+        // the TMA variant's bulk copies are kept to local memory.  Unmeasured
+        // on hardware (one GPU per box this round); T3DES_CU_MULTI_COPY
+        // selects the copy pipeline below instead.
+        if (peer && aligned && !(flags & (T3DES_CU_MULTI_COPY | T3DES_CU_MULTI_STAGE_ALL))) {
+            const int v = c->variant;
+            c->variant = T3DES_CU_VARIANT_BITSLICE_LDG;
+            rc = run_device(c, dir, in + 8 * first, out + 8 * first, count, c->st[0]);
+            c->variant = v;
+            continue;
         }
         // chunk: about 1/8 of the shard, 8..256 MiB, whole warp tiles
         std::uint64_t chunk =

@@ -457,7 +457,7 @@ def test_multi_device_resident_scatter_gather(oracle):
     x = oracle.payload(8 * n)
     src = dev(x)
     arr = (ctypes.c_int * len(devs))(*devs)
-    for flags in (0, 1):
+    for flags in (0, N.MULTI_STAGE_ALL, N.MULTI_COPY):
         dst = torch.empty_like(src)
         rc = N.lib().t3des_cu_ecb_multi_device(arr, len(devs), s, 0, 0, src.data_ptr(), dst.data_ptr(), x.nbytes,
                                                flags)
