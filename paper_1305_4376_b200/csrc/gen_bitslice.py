@@ -174,25 +174,32 @@ def gen_round(circuits) -> list[str]:
     out.append("//   k[48..63] : S = D | 1, for the FMA-pipe form x ^ D = x * S + D")
     out.append("template <int OPT, class KP>")
     out.append("T3_FI void t3_round(uint32_t (&L)[32], const uint32_t (&R)[32], const T3Fk fk, const KP k) {")
+    # per-S-box statement lists; T3_GEN_ORDER (experiments) interleaves them:
+    # "box" (default: one S-box after the other), "rr" (gate i of every box in
+    # turn), "pairs" (round-robin within S-box pairs)
+    order = os.environ.get("T3_GEN_ORDER", "box")
+    pre = "" if order == "box" else "s{box}"
+    streams = []
     for box in range(8):
         gates, outs = circuits[box]
-        out.append(f"  {{  // S{box + 1}: {len(gates)} lop3")
+        st = []
         names = {}
+        pf = pre.format(box=box)
         for kvar in range(6):
             j = 6 * box + 5 - kvar
             q = E[j] - 1
             if j in d_index:
-                nm = f"x{kvar}"
+                nm = f"{pf}x{kvar}"
                 if (DFMA_MASK >> d_index[j]) & 1:
-                    out.append(f"    const uint32_t {nm} = t3_dfix<OPT>(R[{q}], k[{32 + d_index[j]}], k[{48 + d_index[j]}]);")
+                    st.append(f"const uint32_t {nm} = t3_dfix<OPT>(R[{q}], k[{32 + d_index[j]}], k[{48 + d_index[j]}]);")
                 else:  # kept on the ALU pipe (T3_GEN_DFMA_MASK experiments)
-                    out.append(f"    const uint32_t {nm} = R[{q}] ^ k[{32 + d_index[j]}];")
+                    st.append(f"const uint32_t {nm} = R[{q}] ^ k[{32 + d_index[j]}];")
                 names[kvar] = nm
             else:
                 names[kvar] = f"R[{q}]"
         for g, a, b, c, lut in gates:
-            out.append(f"    const uint32_t g{g} = lop3<0x{lut:02x}>({names[a]}, {names[b]}, {names[c]});")
-            names[g] = f"g{g}"
+            st.append(f"const uint32_t {pf}g{g} = lop3<0x{lut:02x}>({names[a]}, {names[b]}, {names[c]});")
+            names[g] = f"{pf}g{g}"
         for o in range(4):
             pos = 4 * box + 4 - o  # FIPS position in the 32-bit S output
             p = pos_to_p[pos]
@@ -200,11 +207,25 @@ def gen_round(circuits) -> list[str]:
                 # Feistel top: the output's last step h(a, b) merges into the
                 # Feistel lop3; C moves to the FMA pipe (t3_cfix, 2 IMAD).
                 _, a, b, h = outs[o]
-                out.append(f"    L[{p}] = t3_cfix(lop3<0x{feistel_lut(h):02x}>(L[{p}], {names[a]}, {names[b]}), k[{p}], fk);")
+                st.append(f"L[{p}] = t3_cfix(lop3<0x{feistel_lut(h):02x}>(L[{p}], {names[a]}, {names[b]}), k[{p}], fk);")
                 continue
             g, inv = outs[o]
             lut = 0x69 if inv else 0x96  # a^b^c (or its complement)
-            out.append(f"    L[{p}] = lop3<0x{lut:02x}>(L[{p}], {names[g]}, k[{p}]);")
+            st.append(f"L[{p}] = lop3<0x{lut:02x}>(L[{p}], {names[g]}, k[{p}]);")
+        streams.append((box, len(gates), st))
+    if order == "box":
+        for box, ng, st in streams:
+            out.append(f"  {{  // S{box + 1}: {ng} lop3")
+            out += ["    " + x for x in st]
+            out.append("  }")
+    else:
+        groups = [streams] if order == "rr" else [streams[i:i + 2] for i in range(0, 8, 2)]
+        out.append(f"  {{  // S-boxes interleaved ({order})")
+        for grp in groups:
+            for i in range(max(len(st) for _, _, st in grp)):
+                for _, _, st in grp:
+                    if i < len(st):
+                        out.append("    " + st[i])
         out.append("  }")
     out.append("}")
     return out
