@@ -552,6 +552,27 @@ def _splitmix_checksum(e, torch, n) -> int:
 
 
 
+def e2e_multi(torch, N, ts, host, one: int, world: int, ndev: int, k3: int) -> dict:
+    """One process driving all N GPUs through t3des_cu_ecb_multi (the
+    workers axis of DispatchConfig) on a pinned buffer of N x `one` bytes."""
+    devs = [r % max(ndev, 1) for r in range(world)]
+    mh = torch.empty(world * one, dtype=torch.uint8).pin_memory()
+    for r in range(world):
+        mh[r * one:(r + 1) * one].copy_(host)
+    cdevs = (ctypes.c_int * world)(*devs)
+    sub = ts.sub48()
+    f = N.lib().t3des_cu_ecb_multi
+    rc = f(cdevs, world, sub, 0, mh.data_ptr(), mh.data_ptr(), mh.numel())
+    t0 = time.perf_counter()
+    for _ in range(k3):
+        rc = rc or f(cdevs, world, sub, 0, mh.data_ptr(), mh.data_ptr(), mh.numel())
+    dtm = (time.perf_counter() - t0) / k3
+    return {"value": round(world * one / dtm / 1e9, 3) if rc == 0 else None, "unit": "GB/s",
+            "devices": devs, "bytes": world * one, "status": N.strerror(rc),
+            "path": "t3des_cu_ecb_multi from one process (one host thread + context per "
+                    "device, pinned buffer), the GPU reading of DispatchConfig.workers"}
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -844,42 +865,36 @@ def main() -> None:
                                    "path": "t3des_cu_ecb_host, pageable host buffer (numpy), in place"}
         # the same pageable buffer after the opt-in t3des_cu_host_register
         # (a caller that reuses its buffer): the pinned DMA path, no staging
-        t0 = time.perf_counter()
-        reg = t3.HostRegistration(page)
-        reg_ms = (time.perf_counter() - t0) * 1e3
-        e.ecb_host(0, page.ctypes.data, page.ctypes.data, one)
+        try:
+            t0 = time.perf_counter()
+            reg = t3.HostRegistration(page)
+            reg_ms = (time.perf_counter() - t0) * 1e3
+            e.ecb_host(0, page.ctypes.data, page.ctypes.data, one)
+            ok_reg = True
+        except Exception as exc:  # an extra leg: never lose the line over it
+            ok_reg, reg_err = False, f"{type(exc).__name__}: {exc}"[:300]
         barrier()
         t0 = time.perf_counter()
-        for _ in range(k3):
+        for _ in range(k3 if ok_reg else 0):
             e.ecb_host(0, page.ctypes.data, page.ctypes.data, one)
         dtr = max_over_ranks((time.perf_counter() - t0) / k3)
-        reg.close()
-        line["e2e"]["pageable_registered"] = {
-            "value": round(world * one / dtr / 1e9, 3), "unit": "GB/s", "register_ms": round(reg_ms, 1),
-            "path": "the pageable buffer registered once with t3des_cu_host_register (opt-in, outside the timing)"}
+        if ok_reg:
+            reg.close()
+            line["e2e"]["pageable_registered"] = {
+                "value": round(world * one / dtr / 1e9, 3), "unit": "GB/s", "register_ms": round(reg_ms, 1),
+                "path": "the pageable buffer registered once with t3des_cu_host_register (opt-in, outside the timing)"}
+        else:
+            line["e2e"]["pageable_registered"] = {"value": None, "error": reg_err}
         del page
         # one process driving all N GPUs through t3des_cu_ecb_multi (the
         # workers axis of DispatchConfig): rank 0, the other ranks idle on a
         # host-side barrier
         host_barrier()
         if rank == 0:
-            devs = [r % max(ndev, 1) for r in range(world)]
-            mh = torch.empty(world * one, dtype=torch.uint8).pin_memory()
-            for r in range(world):
-                mh[r * one:(r + 1) * one].copy_(host)
-            cdevs = (ctypes.c_int * world)(*devs)
-            sub = ts.sub48()
-            f = N.lib().t3des_cu_ecb_multi
-            rc = f(cdevs, world, sub, 0, mh.data_ptr(), mh.data_ptr(), mh.numel())
-            t0 = time.perf_counter()
-            for _ in range(k3):
-                rc = rc or f(cdevs, world, sub, 0, mh.data_ptr(), mh.data_ptr(), mh.numel())
-            dtm = (time.perf_counter() - t0) / k3
-            line["e2e"]["multi"] = {"value": round(world * one / dtm / 1e9, 3) if rc == 0 else None, "unit": "GB/s",
-                                    "devices": devs, "bytes": world * one, "status": N.strerror(rc),
-                                    "path": "t3des_cu_ecb_multi from one process (one host thread + context per "
-                                            "device, pinned buffer), the GPU reading of DispatchConfig.workers"}
-            del mh
+            try:
+                line["e2e"]["multi"] = e2e_multi(torch, N, ts, host, one, world, ndev, k3)
+            except Exception as exc:  # an extra leg: never lose the line over it
+                line["e2e"]["multi"] = {"value": None, "error": f"{type(exc).__name__}: {exc}"[:300]}
         host_barrier()
         del host
     else:
@@ -887,7 +902,11 @@ def main() -> None:
         del src
 
     if not args.no_extra_configs and world == 1:
-        line["configs_measured"] = extra_configs(e, t3, N, torch, np)
+        try:
+            line["configs_measured"] = extra_configs(e, t3, N, torch, np)
+        except Exception as exc:
+            line["configs_measured"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+            torch.cuda.empty_cache()
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_reference_arm()
