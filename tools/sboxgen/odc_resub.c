@@ -56,7 +56,8 @@ typedef struct {
 } circ_t;
 
 static tt_t TARGET[4];
-static long n_neutral = 0, n_gain = 0, n_zero = 0;
+static long n_neutral = 0, n_gain = 0, n_zero = 0, n_two = 0;
+static int g_two = 0; /* 2-resub enabled (ODC_TWO=1): slow, ~1e9 checks per gate */
 static uint64_t rng = 0x9E3779B97F4A7C15ull;
 static uint64_t rnd(void) {
     rng ^= rng << 13;
@@ -269,6 +270,45 @@ static int move(circ_t* c, int g, int p_neutral_pct) {
                     bl = l;
                 }
             }
+    if (best_gain <= 0 && g_two) {
+        /* 2-resub: g' = LUT3(h, x, y), h = LUT3(a, b, c) new, when g's
+         * fanout-free cone has >= 3 gates (gain >= 1) */
+        circ_t t = *c;
+        t.in[g][0] = t.in[g][1] = t.in[g][2] = 0;
+        rebuild(&t);
+        const int mffc = before - gates(&t) + 1;
+        if (mffc >= 3 && c->n < MAXS) {
+            for (int i = 0; i < nc; i++)
+                for (int j = i + 1; j < nc; j++)
+                    for (int k = j + 1; k < nc; k++) {
+                        const tt_t A = c->tt[cand[i]], B = c->tt[cand[j]], C = c->tt[cand[k]];
+                        for (int l = 1; l < 255; l++) {
+                            const tt_t H = lut_eval((uint8_t)l, A, B, C);
+                            for (int x = 0; x < nc; x++)
+                                for (int y = x + 1; y < nc; y++) {
+                                    const int l2 = find_lut3(H, c->tt[cand[x]], c->tt[cand[y]], T, care);
+                                    if (l2 < 0) continue;
+                                    circ_t u = *c;
+                                    const int h = u.n++;
+                                    u.in[h][0] = cand[i];
+                                    u.in[h][1] = cand[j];
+                                    u.in[h][2] = cand[k];
+                                    u.lut[h] = (uint8_t)l;
+                                    u.in[g][0] = h;
+                                    u.in[g][1] = cand[x];
+                                    u.in[g][2] = cand[y];
+                                    u.lut[g] = (uint8_t)l2;
+                                    rebuild(&u);
+                                    if (correct(&u) && gates(&u) < before) {
+                                        *c = u;
+                                        ++n_two;
+                                        return before - gates(c);
+                                    }
+                                }
+                        }
+                    }
+        }
+    }
     if (ba < 0) return 0;
     if (best_gain > 0 || (best_gain == 0 && (int)(rnd() % 100) < p_neutral_pct)) {
         c->in[g][0] = ba;
@@ -303,6 +343,7 @@ int main(int argc, char** argv) {
         fprintf(stderr, "cannot load a correct circuit from %s\n", argv[2]);
         return 1;
     }
+    g_two = getenv("ODC_TWO") && atoi(getenv("ODC_TWO"));
     const int start = gates(&c);
     best = c;
     fprintf(stderr, "box %d: start %d gates\n", box, start);
@@ -316,8 +357,8 @@ int main(int argc, char** argv) {
         }
         if (it % 20000 == 19999) {
             if (gates(&c) > gates(&best)) c = best; /* never happens: moves do not grow */
-            fprintf(stderr, "box %d: iteration %ld, current %d, best %d (neutral %ld, 1-resub gains %ld, 0-resub %ld)\n",
-                    box, it + 1, gates(&c), gates(&best), n_neutral, n_gain, n_zero);
+            fprintf(stderr, "box %d: iteration %ld, current %d, best %d (neutral %ld, 1-resub gains %ld, 0-resub %ld, 2-resub %ld)\n",
+                    box, it + 1, gates(&c), gates(&best), n_neutral, n_gain, n_zero, n_two);
         }
     }
     printf("box %d: %d -> %d gates\n", box, start, gates(&best));
