@@ -368,6 +368,12 @@ class HostRegistration:
     def __exit__(self, *exc):
         self.close()
 
+    def __del__(self):  # pragma: no cover - best effort; holds the buffer alive until here
+        try:
+            self.close()
+        except Exception:
+            pass
+
 
 def encrypt_batch(src, dst, ts: TripleSchedule, cfg: DispatchConfig | None = None) -> None:
     """ECB-encrypt `src` into `dst` (same length, multiple of 8 bytes;
