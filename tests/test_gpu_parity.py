@@ -338,6 +338,16 @@ int main(int argc, char** argv) {
     encrypt_batch(in, out, ts, DispatchConfig{});
     decrypt_batch(out, back, ts, DispatchConfig{});
     if (back != in) return 3;
+    {   // opt-in page-locking of a reused buffer (RAII), and the workers axis
+        std::vector<std::uint8_t> reg(out.size()), again(out.size());
+        HostRegistration r(reg);
+        DispatchConfig two;
+        two.workers = 2;
+        encrypt_batch(in, reg, ts, two);
+        if (reg != out) return 4;
+        decrypt_batch(reg, again, ts, DispatchConfig{});
+        if (again != in) return 5;
+    }
     std::FILE* f = std::fopen(argv[2], "wb");
     std::fwrite(out.data(), 1, out.size(), f);
     std::fclose(f);
