@@ -85,6 +85,17 @@ struct DeviceScope {
     DeviceScope& operator=(const DeviceScope&) = delete;
 };
 
+// In and out spans overlap without being the same span (the reference's
+// InputLengthError case, dispatch.cpp:99-104).
+inline bool partial_overlap(const void* a, const void* b, std::size_t len) {
+    const auto* x = static_cast<const std::uint8_t*>(a);
+    const auto* y = static_cast<const std::uint8_t*>(b);
+    return x != y && y < x + len && y + len > x;
+}
+
+// host copy threads of the pageable staging path (in + out pools)
+constexpr int kMaxCopyThreads = 14;
+
 // Transform nblocks device blocks on stream s (in may equal out), honouring
 // the context's variant and launch shaping.  Returns a T3DES_CU_* status.
 int run_device(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8_t* out, std::uint64_t nblocks,

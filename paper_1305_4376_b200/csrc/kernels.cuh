@@ -31,7 +31,6 @@
 #endif
 #define T3_SP_THREADS 256        // SP-table CTA size for small batches
 #define T3_SP_THREADS_BIG 1024  // ... and for batches of >= 16384 blocks
-#define T3_TILE_BLOCKS 1024  // blocks per warp tile (32 lanes x 32 blocks)
 #ifndef T3_OPT_DEFAULT
 #define T3_OPT_DEFAULT T3_OPT_DFMA  // for the LDG/tail kernels; the TMA kernel's mask is per context
 #endif

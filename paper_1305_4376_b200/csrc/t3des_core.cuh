@@ -13,6 +13,8 @@
 #pragma once
 #include <stdint.h>
 
+#define T3_TILE_BLOCKS 1024  // blocks per warp tile (32 lanes x 32 blocks)
+
 #ifdef __CUDACC__
 #define T3_FI __host__ __device__ __forceinline__
 #else
