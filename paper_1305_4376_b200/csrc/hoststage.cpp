@@ -309,4 +309,48 @@ void Worker::wait() {
     done_cv_.wait(l, [&] { return !busy_; });
 }
 
+PartPool::PartPool(int n) : n_(std::max(1, n)) {
+    th_.reserve(n_ - 1);
+    for (int i = 1; i < n_; ++i) th_.emplace_back([this, i] { loop(i); });
+}
+
+PartPool::~PartPool() {
+    {
+        std::lock_guard<std::mutex> l(m_);
+        stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+}
+
+void PartPool::loop(int part) {
+    std::uint64_t seen = 0;
+    for (;;) {
+        const std::function<void(int, int)>* fn;
+        {
+            std::unique_lock<std::mutex> l(m_);
+            cv_.wait(l, [&] { return stop_ || gen_ != seen; });
+            if (stop_) return;
+            seen = gen_;
+            fn = fn_;
+        }
+        (*fn)(part, n_);
+        std::lock_guard<std::mutex> l(m_);
+        if (--left_ == 0) done_cv_.notify_all();
+    }
+}
+
+void PartPool::run(const std::function<void(int, int)>& fn) {
+    {
+        std::lock_guard<std::mutex> l(m_);
+        fn_ = &fn;
+        left_ = n_ - 1;
+        ++gen_;
+    }
+    cv_.notify_all();
+    fn(0, n_);
+    std::unique_lock<std::mutex> l(m_);
+    done_cv_.wait(l, [&] { return left_ == 0; });
+}
+
 }  // namespace t3b

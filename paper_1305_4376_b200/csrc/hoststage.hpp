@@ -96,6 +96,31 @@ private:
     std::vector<std::thread> th_;
 };
 
+// n persistent threads that run one data-parallel job at a time: run(fn)
+// calls fn(part, n) for part = 0..n-1 (part 0 on the calling thread) and
+// returns when all parts are done.  The stream path's parallel pread/pwrite
+// of regular files uses it.
+class PartPool {
+public:
+    explicit PartPool(int n);
+    ~PartPool();
+    PartPool(const PartPool&) = delete;
+    PartPool& operator=(const PartPool&) = delete;
+    void run(const std::function<void(int, int)>& fn);
+    int size() const { return n_; }
+
+private:
+    void loop(int part);
+    const int n_;
+    std::mutex m_;
+    std::condition_variable cv_, done_cv_;
+    const std::function<void(int, int)>* fn_ = nullptr;
+    std::uint64_t gen_ = 0;
+    int left_ = 0;
+    bool stop_ = false;
+    std::vector<std::thread> th_;
+};
+
 // One persistent thread that runs one job at a time: run() hands it a job
 // and returns; wait() blocks until the job has finished.  The pageable
 // staging path's drain side (copies out of the ring) runs on it, decoupled

@@ -51,8 +51,13 @@ void pkcs7_pad_bytes(std::uint8_t* data, std::size_t len, std::size_t* out_len);
 // Returns the unpadded length; throws StreamFailure{Padding}.
 std::size_t pkcs7_unpad_len(const std::uint8_t* data, std::size_t len);
 
-// The context must hold a schedule.  chunk_blocks >= 1.
+// The context must hold a schedule.  chunk_blocks >= 1.  io_blocks (a
+// multiple of chunk_blocks; 0 = chunk_blocks) is the granularity the source
+// is read, transformed and written in: the output bytes, the padding and the
+// reported chunk count are those of chunk_blocks (the reference's chunks),
+// larger I/O only amortises per-call costs (the fd entry uses it for regular
+// files of known length).
 StreamStats run_stream(t3des_cu_ctx* ctx, int direction, ByteSource& src, ByteSink& dst,
-                       std::size_t chunk_blocks, bool pkcs7);
+                       std::size_t chunk_blocks, bool pkcs7, std::size_t io_blocks = 0);
 
 }  // namespace t3b
