@@ -213,3 +213,40 @@ def test_stream_on_a_non_current_device(ts, oracle):
     mid = io.BytesIO()
     t3.encrypt_stream(io.BytesIO(payload), mid, ts, t3.DispatchConfig(device=1, chunk_blocks=100), t3.PaddingMode.PKCS7)
     assert mid.getvalue() == oracle.ecb(np.frombuffer(t3.pkcs7_pad(payload), np.uint8), oracle.schedule_hex(KEY), 0).tobytes()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("io_mib", [None, "1"])
+def test_regular_file_streams_keep_reference_chunk_semantics(ts, oracle, tmp_path, monkeypatch, io_mib):
+    """The fd entry on regular files (parallel pread/pwrite, I/O pieces of many
+    reference chunks): same bytes, the reference's chunk count, and on a
+    padding error exactly the chunks the reference writes before throwing
+    (every chunk but the last)."""
+    if io_mib:
+        monkeypatch.setenv("T3DES_STREAM_IO_MIB", io_mib)
+    s = oracle.schedule_hex(KEY)
+    cb = 64  # 512-byte reference chunks
+    rng = np.random.default_rng(51)
+    for n in (0, 8, 4096, 3 << 20, (3 << 20) + 5):
+        payload = rng.integers(0, 256, n, dtype=np.uint8).tobytes()
+        src, mid, out = tmp_path / "in", tmp_path / "mid", tmp_path / "out"
+        src.write_bytes(payload)
+        with open(src, "rb") as fi, open(mid, "wb") as fo:
+            r = t3.encrypt_stream(fi.fileno(), fo.fileno(), ts, t3.DispatchConfig(chunk_blocks=cb), t3.PaddingMode.PKCS7)
+            assert fi.tell() == n and fo.tell() == len(t3.pkcs7_pad(payload))  # offsets as sequential I/O leaves them
+        padded = t3.pkcs7_pad(payload)
+        assert mid.read_bytes() == oracle.ecb(np.frombuffer(padded, np.uint8), s, 0).tobytes()
+        assert r.chunks == max(1, -(-n // (8 * cb))) and r.bytes_in == n and r.bytes_out == len(padded)
+        with open(mid, "rb") as fi, open(out, "wb") as fo:
+            t3.decrypt_stream(fi.fileno(), fo.fileno(), ts, t3.DispatchConfig(chunk_blocks=cb), t3.PaddingMode.PKCS7)
+        assert out.read_bytes() == payload
+    # bad padding: a multi-chunk ciphertext whose plaintext ends without padding
+    body = rng.integers(0, 256, 8 * cb * 37 + 8 * 5, dtype=np.uint8)
+    body[-1] = 0  # pad byte 0 is invalid
+    ct = oracle.ecb(body, s, 0).tobytes()
+    src.write_bytes(ct)
+    with open(src, "rb") as fi, open(out, "wb") as fo:
+        with pytest.raises(t3.PaddingError):
+            t3.decrypt_stream(fi.fileno(), fo.fileno(), ts, t3.DispatchConfig(chunk_blocks=cb), t3.PaddingMode.PKCS7)
+    written = out.read_bytes()
+    assert written == body[: 8 * cb * 37].tobytes()  # the 37 full chunks before the last (5-block) one
