@@ -188,7 +188,17 @@ StreamStats run_stream(t3des_cu_ctx* c, int dir, ByteSource& src, ByteSink& dst,
                                                "for arbitrary lengths)"));
             }
         } else if (n % 8) {
-            fail_after_drain(StreamFailure(StreamFailure::Length, "ciphertext length not a multiple of 8"));
+            const StreamFailure f(StreamFailure::Length, "ciphertext length not a multiple of 8");
+            if (!pkcs7) fail_after_drain(f);
+            // PKCS#7: the reference holds each decrypted chunk back until the
+            // next one is read, so the chunk before this one is never written
+            drain(1);
+            if (!inflight.empty()) {
+                (void)cudaStreamSynchronize(c->st[inflight.front().idx]);
+                (void)cudaGetLastError();
+                inflight.clear();
+            }
+            throw f;
         }
         if (n) {
             auto t0 = Clock::now();

@@ -250,3 +250,25 @@ def test_regular_file_streams_keep_reference_chunk_semantics(ts, oracle, tmp_pat
             t3.decrypt_stream(fi.fileno(), fo.fileno(), ts, t3.DispatchConfig(chunk_blocks=cb), t3.PaddingMode.PKCS7)
     written = out.read_bytes()
     assert written == body[: 8 * cb * 37].tobytes()  # the 37 full chunks before the last (5-block) one
+
+
+@pytest.mark.gpu
+def test_decrypt_length_error_output_matches_reference(ts, oracle, tmp_path):
+    """A ciphertext whose length is not a multiple of 8, PKCS#7 decrypt: the
+    reference (dispatch.cpp:111-206) holds each decrypted chunk back until
+    the next is read, so when the short last chunk throws InputLengthError
+    it has written every chunk but the last two."""
+    s = oracle.schedule_hex(KEY)
+    cb = 16
+    body = np.random.default_rng(52).integers(0, 256, 8 * cb * 9, dtype=np.uint8)
+    ct = oracle.ecb(body, s, 0).tobytes() + b"\x01\x02\x03"  # 9 full chunks + 3 stray bytes
+    src, out = tmp_path / "ct", tmp_path / "pt"
+    src.write_bytes(ct)
+    with open(src, "rb") as fi, open(out, "wb") as fo:
+        with pytest.raises(t3.InputLengthError):
+            t3.decrypt_stream(fi.fileno(), fo.fileno(), ts, t3.DispatchConfig(chunk_blocks=cb), t3.PaddingMode.PKCS7)
+    assert out.read_bytes() == body[: 8 * cb * 8].tobytes()
+    with open(src, "rb") as fi, open(out, "wb") as fo:  # without padding: every full chunk
+        with pytest.raises(t3.InputLengthError):
+            t3.decrypt_stream(fi.fileno(), fo.fileno(), ts, t3.DispatchConfig(chunk_blocks=cb), t3.PaddingMode.NONE)
+    assert out.read_bytes() == body.tobytes()
