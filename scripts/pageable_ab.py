@@ -18,8 +18,8 @@ KEY = "133457799BBCDFF10E329232EA6D0D737CA110454A1A6E57"
 x = np.random.default_rng(1).integers(0, 256, GiB, dtype=np.uint8)
 y = np.empty_like(x)
 ts = t3.triple_schedule(t3.parse_hex_key(KEY))
-CONFIGS = [(1, 1, 4, 12), (0, 1, 5, 12), (0, 1, 6, 12), (0, 1, 6, 14), (0, 1, 6, 16), (0, 1, 7, 12), (0, 1, 8, 14),
-           (1, 1, 6, 12)]
+CONFIGS = [(1, 1, 4, 12), (1, 1, 6, 14), (0, 1, 6, 14), (0, 1, 4, 12),
+           (0, 0, 6, 14)]
 engines = {}
 for c in CONFIGS:
     nt_in, nt_out, stage, th = c
