@@ -425,11 +425,12 @@ def extra_configs(e, t3, N, torch, np) -> dict:
         for _ in range(50):
             e.ecb_device(0, d.data_ptr(), y.data_ptr(), x.nbytes, gs.cuda_stream)
             e.ecb_device(1, y.data_ptr(), z.data_ptr(), x.nbytes, gs.cuda_stream)
-    g.replay()
-    torch.cuda.synchronize()
-    ev0.record(gs)
-    g.replay()
-    ev1.record(gs)
+    with torch.cuda.stream(gs):  # replay() launches on the current stream
+        g.replay()
+        torch.cuda.synchronize()
+        ev0.record(gs)
+        g.replay()
+        ev1.record(gs)
     torch.cuda.synchronize()
     us_graph = ev0.elapsed_time(ev1) * 1e3 / 50
     ok = ok and bool(torch.equal(z, d))
