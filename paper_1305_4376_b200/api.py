@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import ctypes
 import enum
+import threading
 from dataclasses import dataclass, field
 
 from . import _native as N
@@ -253,13 +254,19 @@ class Engine:
         return out.value
 
 
-_engines: dict[int, Engine] = {}
+_engines = threading.local()  # one context per device per thread (a context has one submitter at a time)
 
 
 def engine(device: int = 0) -> Engine:
-    e = _engines.get(device)
+    """The calling thread's context for `device` (created on first use).
+    Per thread, like the C++ mirror's context cache: the batch functions stay
+    callable from several threads at once, as the reference's are."""
+    cache = getattr(_engines, "by_device", None)
+    if cache is None:
+        cache = _engines.by_device = {}
+    e = cache.get(device)
     if e is None:
-        e = _engines[device] = Engine(device)
+        e = cache[device] = Engine(device)
     return e
 
 

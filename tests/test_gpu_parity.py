@@ -597,6 +597,42 @@ def test_cuda_graph_capture_and_replay(eng, oracle, variant):
         assert torch.equal(z, src), n
 
 
+def test_batch_api_from_several_threads(oracle):
+    """The batch functions are callable from several host threads at once
+    (each thread gets its own context, like the reference's stateless
+    encrypt_batch): 6 threads x mixed sizes, pageable and device buffers."""
+    import threading
+
+    s = oracle.schedule_hex(KEYS[0])
+    ts = t3.triple_schedule(t3.parse_hex_key(KEYS[0]))
+    errors = []
+
+    def work(i):
+        try:
+            rng = np.random.default_rng(300 + i)
+            for _ in range(8):
+                n = int(rng.integers(1, 300_000))
+                x = rng.integers(0, 256, 8 * n, dtype=np.uint8)
+                y = np.empty_like(x)
+                t3.encrypt_batch(x, y, ts)
+                if not np.array_equal(y, oracle.ecb(x, s, 0)):
+                    errors.append((i, n, "host"))
+                d = torch.from_numpy(y).cuda()
+                t3.decrypt_batch(d, d, ts)
+                torch.cuda.current_stream().synchronize()
+                if not np.array_equal(d.cpu().numpy(), x):
+                    errors.append((i, n, "device"))
+        except Exception as exc:  # noqa: BLE001
+            errors.append((i, repr(exc)))
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(6)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
+
+
 def test_auto_variant_with_large_work_group(eng, oracle):
     """AUTO + a 256-thread work group: small launches use it on the SP-table
     kernel, large ones clamp it to the bitsliced kernel's 128 threads."""
