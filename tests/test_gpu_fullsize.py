@@ -172,3 +172,39 @@ def test_configs3_64gib_whole_output_and_shard_edges(eng, oracle):
         first, count = shard_range(n, 8, r)
         k0, k1 = first >> 27, (first + count) >> 27
         assert eng.checksum(buf.data_ptr() + 8 * first, first, count, st) == sum(pieces[k0:k1]) % 2**64
+
+
+def _enc_dev(e, hexkey, x_dev, direction=0):
+    return device_ecb(e, hexkey, x_dev, direction, N.VARIANT_AUTO)
+
+
+def test_complementation_property_at_full_size(eng):
+    """DES's complementation property carried through EDE: E_{~k}(~x) = ~E_k(x)
+    (reference test_des.cpp "complementation property"), on the full 1 GiB
+    configs[1] payload — a size-independent check of every output bit."""
+    n = GiB // 8
+    x = torch.empty(8 * n, dtype=torch.uint8, device="cuda")
+    eng.fill_splitmix(x.data_ptr(), 0, n, SEED)
+    k = BENCH_KEY
+    nk = "".join(f"{0xF - int(ch, 16):X}" for ch in k)  # every key bit complemented
+    y = _enc_dev(eng, k, x)
+    y2 = _enc_dev(eng, nk, torch.bitwise_not(x))
+    assert torch.equal(torch.bitwise_not(y), y2)
+
+
+@pytest.mark.parametrize("k1,k2", [("0101010101010101", "0101010101010101"),
+                                   ("FEFEFEFEFEFEFEFE", "FEFEFEFEFEFEFEFE"),
+                                   ("01FE01FE01FE01FE", "FE01FE01FE01FE01"),
+                                   ("1FE01FE00EF10EF1", "E01FE01FF10EF10E")])
+def test_weak_and_semi_weak_keys_at_full_size(eng, k1, k2):
+    """Weak keys make (single-DES-equivalent, option 3) encryption an
+    involution, and a semi-weak pair makes E_k2(E_k1(x)) = x (reference
+    test_des.cpp "weak keys make encryption an involution"; FIPS 74) — on
+    1 GiB through the collapsed 16-round path."""
+    n = GiB // 8
+    x = torch.empty(8 * n, dtype=torch.uint8, device="cuda")
+    eng.fill_splitmix(x.data_ptr(), 0, n, SEED + 1)
+    y = _enc_dev(eng, k1, x)
+    assert not torch.equal(y, x)
+    z = _enc_dev(eng, k2, y)
+    assert torch.equal(z, x)
