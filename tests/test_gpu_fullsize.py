@@ -16,6 +16,8 @@ says so in its id.
               (tests/golden/c3_checksum.json), and every block of the tiles
               around each shard boundary of N = 2/4/8 and every 2 GiB
               (64-bit offsets) against the oracle
+  properties  complementation E_~k(~x) = ~E_k(x) and weak / semi-weak key
+              involutions, on the full 1 GiB payload
 """
 import hashlib
 import json
