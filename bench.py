@@ -569,8 +569,6 @@ def _splitmix_checksum(e, torch, n) -> int:
     return v
 
 
-
-
 def e2e_multi(torch, N, ts, host, one: int, world: int, ndev: int, k3: int) -> dict:
     """One process driving all N GPUs through t3des_cu_ecb_multi (the
     workers axis of DispatchConfig) on a pinned buffer of N x `one` bytes."""
