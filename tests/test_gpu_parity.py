@@ -484,6 +484,29 @@ def test_multi_device_resident_scatter_gather(oracle):
     assert rc == 0 and np.array_equal(b[5: 5 + x.nbytes].cpu().numpy(), oracle.ecb(x, s, 0))
 
 
+@pytest.mark.parametrize("flags", [0, N.MULTI_COPY, N.MULTI_STAGE_ALL])
+def test_multi_device_on_real_peers(oracle, flags):
+    """ecb_multi_device across distinct GPUs (skipped on one-GPU boxes): the
+    remote shards run peer-direct over NVLink (flags 0) or through the chunked
+    peer-copy pipeline (MULTI_COPY, STAGE_ALL); bytes equal the oracle."""
+    ngpu = torch.cuda.device_count()
+    if ngpu < 2:
+        pytest.skip("needs two or more GPUs")
+    devs = list(range(min(ngpu, 8)))
+    s = oracle.schedule_hex(KEYS[0])
+    n = 1024 * 257 * len(devs) + 13
+    x = oracle.splitmix(11, n, 0x9E)
+    src = dev(x)
+    dst = torch.empty_like(src)
+    arr = (ctypes.c_int * len(devs))(*devs)
+    assert N.lib().t3des_cu_ecb_multi_device(arr, len(devs), s, 0, 0, src.data_ptr(), dst.data_ptr(), x.nbytes,
+                                             flags) == 0
+    assert np.array_equal(host(dst), oracle.ecb(x, s, 0))
+    assert N.lib().t3des_cu_ecb_multi_device(arr, len(devs), s, 1, 0, dst.data_ptr(), dst.data_ptr(), x.nbytes,
+                                             flags) == 0
+    assert torch.equal(dst, src)
+
+
 @pytest.mark.parametrize("home_share", [None, "0.2", "0.5"])
 def test_multi_device_weighted_home_shard(oracle, monkeypatch, home_share):
     """ecb_multi_device with a weighted home shard (T3DES_MULTI_HOME_SHARE
