@@ -625,7 +625,6 @@ int t3des_cu_destroy(t3des_cu_ctx* c) {
         delete c->pool_out;
         delete c->drain;
         delete c->io_pool;
-        delete c->io_pool_w;
         if (c->d_sp) cudaFree(c->d_sp);
         if (c->d_acc) cudaFree(c->d_acc);
         (void)cudaGetLastError();

@@ -55,8 +55,7 @@ struct t3des_cu_ctx {
     t3b::CopyPool* pool_in = nullptr;
     t3b::CopyPool* pool_out = nullptr;
     t3b::Worker* drain = nullptr;  // drain side of the pageable ring (copies out)
-    t3b::PartPool* io_pool = nullptr;    // parallel pread of the stream fd entry
-    t3b::PartPool* io_pool_w = nullptr;  // ... and pwrite (the writes run on the worker thread)
+    t3b::PartPool* io_pool = nullptr;  // parallel pread/pwrite of the stream fd entry
     int host_slots = 4;            // pinned ring slots in use (<= kHostSlots)
     std::size_t stage_bytes = std::size_t(6) << 20;  // pageable stage size (scripts/pageable_ab.py)
     int copy_threads = 0;                            // total host copy threads (0 = auto)

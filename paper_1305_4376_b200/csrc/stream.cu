@@ -27,31 +27,23 @@ using Clock = std::chrono::steady_clock;
 
 double since(Clock::time_point t0) { return std::chrono::duration<double>(Clock::now() - t0).count(); }
 
-// Ring slots: chunk k+1 is read into one while chunk k is on the GPU and
-// chunk k-1 is completed (3); with asynchronous writes a fourth slot holds
-// the chunk whose write is still in flight.
-constexpr int kMaxSlots = 4;
+constexpr int kSlots = 3;
 
 // Pinned host ring for the stream pipeline.
 struct PinnedRing {
-    std::uint8_t* p[kMaxSlots] = {};
-    int n;
-    PinnedRing(std::size_t bytes, int slots) : n(slots) {
-        for (int i = 0; i < n; ++i)
-            if (cudaHostAlloc(reinterpret_cast<void**>(&p[i]), bytes, cudaHostAllocDefault) != cudaSuccess) {
+    std::uint8_t* p[kSlots] = {};
+    explicit PinnedRing(std::size_t bytes) {
+        for (auto& x : p)
+            if (cudaHostAlloc(reinterpret_cast<void**>(&x), bytes, cudaHostAllocDefault) != cudaSuccess) {
                 (void)cudaGetLastError();
-                p[i] = nullptr;
+                x = nullptr;
             }
     }
     ~PinnedRing() {
         for (auto* x : p)
             if (x) cudaFreeHost(x);
     }
-    bool ok() const {
-        for (int i = 0; i < n; ++i)
-            if (!p[i]) return false;
-        return true;
-    }
+    bool ok() const { return p[0] && p[1] && p[2]; }
 };
 
 struct Slot {
@@ -97,18 +89,15 @@ StreamStats run_stream(t3des_cu_ctx* c, int dir, ByteSource& src, ByteSink& dst,
     if (io_blocks < chunk_blocks || io_blocks % chunk_blocks) io_blocks = chunk_blocks;
     const std::size_t chunk = io_blocks * 8;  // I/O + transform granularity
     const bool enc = dir == T3DES_CU_ENCRYPT;
-    const int kSlots = async_write ? 4 : 3;
-    PinnedRing ring(chunk + 8, kSlots);
+    PinnedRing ring(chunk + 8);
     if (!ring.ok()) throw StreamFailure(StreamFailure::Cuda, "pinned staging allocation failed", 0, T3DES_CU_ERR_CUDA);
     if (int rc = ensure_staging(c, chunk + 8, kSlots))
         throw StreamFailure(StreamFailure::Cuda, t3des_cu_strerror(rc), 0, rc);
 
     // Asynchronous writes (fd entry): a completed chunk's bytes are written
     // by c->drain while this thread reads the next chunk and queues its GPU
-    // work.  At most one write is in flight: completing chunk k-2 first waits
-    // for chunk k-3's write, whose slot is the one chunk k+1 is then read
-    // into (4 slots: k+1 reading, k and k-1 on the GPU... see drain(1)
-    // below).  The guard waits for the writer on every exit.
+    // work; at most one write is in flight and never on a slot being refilled
+    // (see drain(kSlots - 2) below).  The guard waits for it on every exit.
     t3b::Worker* writer = nullptr;
     if (async_write) {
         if (!c->drain) c->drain = new t3b::Worker();
@@ -229,7 +218,7 @@ StreamStats run_stream(t3des_cu_ctx* c, int dir, ByteSource& src, ByteSink& dst,
         std::size_t next_got = 0;
         const int nslot = (k + 1) % kSlots;
         if (got == chunk) {
-            drain(1);  // chunk k-1 stays in flight; the slot of chunk k+1 is free (and written out)
+            drain(kSlots - 2);
             try {
                 next_got = timed_read(nslot);
             } catch (const StreamFailure& f) {
@@ -409,12 +398,9 @@ extern "C" int t3des_cu_stream_fd(t3des_cu_ctx* c, int dir, int in_fd, int out_f
     // (whole reference chunks) when the input's length is known to be valid
     // — a length error must surface after exactly the chunks the reference
     // writes first, which the chunk-by-chunk loop reproduces.
-    // separate pools: reads (this thread) and writes (the worker) run at once
-    const int io_threads = std::clamp(t3b::available_cpus() / 4, 1, 4);
-    if (!c->io_pool) c->io_pool = new t3b::PartPool(io_threads);
-    if (!c->io_pool_w) c->io_pool_w = new t3b::PartPool(io_threads);
+    if (!c->io_pool) c->io_pool = new t3b::PartPool(std::clamp(t3b::available_cpus() / 2, 1, 8));
     FdSource src(in_fd, c->io_pool);
-    FdSink dst(out_fd, c->io_pool_w);
+    FdSink dst(out_fd, c->io_pool);
     std::size_t io_blocks = chunk_blocks;
     const bool len_ok = src.par && (src.size - src.pos) % 8 == 0;
     if (src.par && (len_ok || (dir == T3DES_CU_ENCRYPT && pkcs7))) {
