@@ -13,7 +13,6 @@
 #include <chrono>
 #include <cstring>
 #include <deque>
-#include <exception>
 #include <vector>
 
 #include "ctx.hpp"
@@ -82,7 +81,7 @@ std::size_t pkcs7_unpad_len(const std::uint8_t* data, std::size_t len) {
 }
 
 StreamStats run_stream(t3des_cu_ctx* c, int dir, ByteSource& src, ByteSink& dst, std::size_t chunk_blocks,
-                       bool pkcs7, std::size_t io_blocks, bool async_write) {
+                       bool pkcs7, std::size_t io_blocks) {
     DeviceScope scope(c->device);  // the ring, staging and streams live on the context's device
     StreamStats st;
     const std::size_t logical = chunk_blocks * 8;  // the reference's chunk
@@ -93,35 +92,6 @@ StreamStats run_stream(t3des_cu_ctx* c, int dir, ByteSource& src, ByteSink& dst,
     if (!ring.ok()) throw StreamFailure(StreamFailure::Cuda, "pinned staging allocation failed", 0, T3DES_CU_ERR_CUDA);
     if (int rc = ensure_staging(c, chunk + 8, kSlots))
         throw StreamFailure(StreamFailure::Cuda, t3des_cu_strerror(rc), 0, rc);
-
-    // Asynchronous writes (fd entry): a completed chunk's bytes are written
-    // by c->drain while this thread reads the next chunk and queues its GPU
-    // work; at most one write is in flight and never on a slot being refilled
-    // (see drain(kSlots - 2) below).  The guard waits for it on every exit.
-    t3b::Worker* writer = nullptr;
-    if (async_write) {
-        if (!c->drain) c->drain = new t3b::Worker();
-        writer = c->drain;
-    }
-    std::exception_ptr werr;
-    double wsecs = 0;
-    struct WriterGuard {
-        t3b::Worker* w;
-        ~WriterGuard() {
-            if (w) w->wait();
-        }
-    } wguard{writer};
-    auto wait_writer = [&] {
-        if (!writer) return;
-        writer->wait();
-        st.io_seconds += wsecs;
-        wsecs = 0;
-        if (werr) {
-            auto e = werr;
-            werr = nullptr;
-            std::rethrow_exception(e);
-        }
-    };
 
     std::deque<Slot> inflight;
     auto complete = [&](const Slot& s) {
@@ -140,29 +110,12 @@ StreamStats run_stream(t3des_cu_ctx* c, int dir, ByteSource& src, ByteSink& dst,
                 // padding is bad: with I/O coarser than its chunks, write the
                 // leading logical chunks of this slot first
                 const std::size_t head = s.n ? (s.n - 1) / logical * logical : 0;
-                wait_writer();
                 if (head) dst.write(ring.p[s.idx], head);
                 st.bytes_out += head;
                 throw;
             }
         }
-        if (n && writer) {
-            wait_writer();
-            const std::uint8_t* p = ring.p[s.idx];
-            const std::uint64_t off = st.bytes_out;
-            writer->run([&, p, n, off] {
-                const auto w0 = Clock::now();
-                try {
-                    dst.write(p, n);
-                } catch (const StreamFailure&) {
-                    werr = std::current_exception();
-                } catch (const std::exception&) {
-                    werr = std::make_exception_ptr(StreamFailure(StreamFailure::Io, "write failure", off));
-                }
-                wsecs = since(w0);
-            });
-            st.bytes_out += n;
-        } else if (n) {
+        if (n) {
             t0 = Clock::now();
             try {
                 dst.write(ring.p[s.idx], n);
@@ -184,7 +137,6 @@ StreamStats run_stream(t3des_cu_ctx* c, int dir, ByteSource& src, ByteSink& dst,
     };
     auto fail_after_drain = [&](const StreamFailure& f) {
         drain(0);  // the reference has written every earlier chunk when it throws
-        wait_writer();
         throw f;
     };
     auto timed_read = [&](int slot) -> std::size_t {
@@ -270,7 +222,6 @@ StreamStats run_stream(t3des_cu_ctx* c, int dir, ByteSource& src, ByteSink& dst,
         ++k;
     }
     drain(0);
-    wait_writer();
     if (!enc && pkcs7 && st.bytes_in == 0)
         throw StreamFailure(StreamFailure::Padding, "empty ciphertext cannot carry PKCS#7 padding");
     if (chunk != logical)  // report the reference's chunk count
@@ -410,7 +361,7 @@ extern "C" int t3des_cu_stream_fd(t3des_cu_ctx* c, int dir, int in_fd, int out_f
     if (const char* e = std::getenv("T3DES_STREAM_IO_MIB"))  // experiments
         io_blocks = std::max<std::size_t>(1, (std::size_t(std::atoi(e)) << 17) / chunk_blocks) * chunk_blocks;
     try {
-        const t3b::StreamStats s = t3b::run_stream(c, dir, src, dst, chunk_blocks, pkcs7 != 0, io_blocks, true);
+        const t3b::StreamStats s = t3b::run_stream(c, dir, src, dst, chunk_blocks, pkcs7 != 0, io_blocks);
         if (report) {
             report->bytes_in = s.bytes_in;
             report->bytes_out = s.bytes_out;

@@ -57,10 +57,7 @@ std::size_t pkcs7_unpad_len(const std::uint8_t* data, std::size_t len);
 // reported chunk count are those of chunk_blocks (the reference's chunks),
 // larger I/O only amortises per-call costs (the fd entry uses it for regular
 // files of known length).
-// async_write: completed chunks are written by the context's worker thread
-// while the next chunk is read (the fd entry; the sink must tolerate being
-// written from that thread).
 StreamStats run_stream(t3des_cu_ctx* ctx, int direction, ByteSource& src, ByteSink& dst,
-                       std::size_t chunk_blocks, bool pkcs7, std::size_t io_blocks = 0, bool async_write = false);
+                       std::size_t chunk_blocks, bool pkcs7, std::size_t io_blocks = 0);
 
 }  // namespace t3b
