@@ -37,6 +37,14 @@ def _worker(rank: int, world: int, port: int, nblocks: int, q):
         y = o.ecb(x, s, 0, threads=1)
         cs = torch.tensor([checksum(y, first) & ((1 << 63) - 1), checksum(y, first) >> 63], dtype=torch.int64)
         dist.all_reduce(cs, op=dist.ReduceOp.SUM)
+        # bench.py's form: each rank's u64 checksum as a signed int64,
+        # all_gather, sum mod 2^64 on the receiver
+        import bench
+
+        mine = torch.tensor([bench.u64_to_i64(checksum(y, first))], dtype=torch.int64)
+        parts = [torch.zeros_like(mine) for _ in range(world)]
+        dist.all_gather(parts, mine)
+        bench_sum = sum(int(p.item()) for p in parts) % 2**64
         bounds = torch.tensor([first, count], dtype=torch.int64)
         gathered = [torch.zeros(2, dtype=torch.int64) for _ in range(world)]
         dist.all_gather(gathered, bounds)
@@ -45,7 +53,7 @@ def _worker(rank: int, world: int, port: int, nblocks: int, q):
         t = torch.tensor([float(rank + 1)], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         if rank == 0:
-            q.put((cs.tolist(), [g.tolist() for g in gathered], b"".join(outs), float(t.item())))
+            q.put((cs.tolist(), [g.tolist() for g in gathered], b"".join(outs), float(t.item()), bench_sum))
     finally:
         dist.destroy_process_group()
 
@@ -59,7 +67,7 @@ def test_two_rank_block_range_sharding(nblocks):
     procs = [ctx.Process(target=_worker, args=(r, world, port, nblocks, q)) for r in range(world)]
     for p in procs:
         p.start()
-    cs, bounds, joined, tmax = q.get(timeout=120)
+    cs, bounds, joined, tmax, bench_sum = q.get(timeout=120)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -75,6 +83,7 @@ def test_two_rank_block_range_sharding(nblocks):
     assert joined == whole.tobytes()
     full = checksum(whole, 0)
     assert ((cs[1] << 63) + cs[0]) % 2**64 == full
+    assert bench_sum == full
     assert tmax == 2.0
 
 
