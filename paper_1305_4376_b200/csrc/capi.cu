@@ -2,8 +2,10 @@
 //
 // Owns: device selection, per-context streams and staging buffers, the
 // host-flattened key tables, kernel launch shaping, the pipelined
-// host-buffer path and the multi-GPU block-range sharding.  No exception
-// crosses this boundary and there is no CPU fallback.
+// host-buffer paths (pinned DMA pipeline, zero-copy, pageable staging) and
+// the utility entries; the multi-GPU entries are in multi.cu, the stream
+// entry in stream.cu.  No exception crosses this boundary and there is no
+// CPU fallback.
 #include <cuda_runtime.h>
 
 #include <algorithm>
