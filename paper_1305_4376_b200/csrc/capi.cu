@@ -343,15 +343,12 @@ int ecb_host_staged(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8
         // profiles/r2/pageable_ab_r2k*.txt): 14 threads with 6 MiB stages and
         // cached stores into the slots are best
         if (total <= 0) total = std::clamp(t3b::available_cpus() * 7 / 8, 2, kMaxCopyThreads);
-        // Copies into the pinned slots use ordinary (cached) stores: the slot
-        // stays in the CPU's last-level cache, where the H2D DMA reads it
-        // (DDIO) instead of from DRAM — +8-17% end to end over streaming
-        // stores (profiles/r2/pageable_ab_r2k*.txt).  Copies out to the
-        // caller's buffer use streaming stores (no read-for-ownership; the
-        // caller's data is not re-read by this thread).  Overrides for
-        // experiments: T3DES_HOST_NT_IN / T3DES_HOST_NT_OUT.
+        // Copies out to the caller's buffer use streaming stores (no
+        // read-for-ownership; the caller's data is not re-read by this
+        // thread).  Copies into the pinned slots choose per batch (below).
+        // Overrides for experiments: T3DES_HOST_NT_IN / T3DES_HOST_NT_OUT.
         auto flag = [](const char* n, bool d) { const char* e = std::getenv(n); return e ? std::atoi(e) != 0 : d; };
-        c->pool_in = new t3b::CopyPool((total + 1) / 2, node, flag("T3DES_HOST_NT_IN", false));
+        c->pool_in = new t3b::CopyPool((total + 1) / 2, node, flag("T3DES_HOST_NT_IN", true));
         c->pool_out = new t3b::CopyPool(std::max(1, total / 2), node, flag("T3DES_HOST_NT_OUT", true));
     }
     const std::size_t nst = (len + S - 1) / S;
@@ -384,6 +381,14 @@ int ecb_host_staged(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8
     if (const char* e = std::getenv("T3DES_ZEROCOPY_MAX")) zc_max = std::strtoull(e, nullptr, 10);  // experiments
     const bool zc = !in_pinned && !out_pinned && len <= zc_max && !c->chunk_blocks &&
                     (c->variant == T3DES_CU_VARIANT_AUTO || c->variant == T3DES_CU_VARIANT_SPTABLE);
+    // Slot-store policy of the fill side: batches of >= 256 MiB copy into
+    // the slots with ordinary (cached) stores, so a slot is still in the
+    // CPU's last-level cache when the H2D DMA reads it (DDIO) — 1 GiB 29.6
+    // vs 27.0 GB/s; smaller batches use streaming stores — 16 MiB 17.9 vs
+    // 12.9, 64 MiB 23.5 vs 19.1 — (profiles/r2/pageable_policy_r2t.txt;
+    // 128 MiB is the crossover).  T3DES_HOST_NT_IN overrides.
+    int in_streaming = len >= (std::size_t(256) << 20) ? 0 : 1;
+    if (std::getenv("T3DES_HOST_NT_IN")) in_streaming = -1;  // the pool default set from the variable
     // Fill side (this thread) and drain side (c->drain) run decoupled over the
     // ring of R slots: the fill side copies stage k into slot k % R once the
     // drain side has released it, then enqueues H2D -> kernel -> D2H (or the
@@ -430,7 +435,7 @@ int ecb_host_staged(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8
             if (stop) break;
         }
         if (!in_pinned) {  // the slot's last stage has been copied out (or DMA'd to a pinned out)
-            c->pool_in->start(c->hbuf[slot], in + off(k), cnt(k));
+            c->pool_in->start(c->hbuf[slot], in + off(k), cnt(k), in_streaming);
             c->pool_in->wait();
         }
         cudaStream_t s = c->st[slot];

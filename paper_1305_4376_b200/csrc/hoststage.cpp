@@ -205,7 +205,10 @@ void host_free_on_node(void* p, std::size_t bytes, bool registered) {
 }
 
 CopyPool::CopyPool(int nthreads, NumaNode node, bool streaming)
-    : n_(std::max(1, nthreads)), node_(std::move(node)), nt_(streaming && env_flag("T3DES_HOST_NT_COPY", true)) {
+    : n_(std::max(1, nthreads)),
+      node_(std::move(node)),
+      nt_allowed_(env_flag("T3DES_HOST_NT_COPY", true)),
+      nt_(streaming && nt_allowed_) {
     th_.reserve(n_);
     for (int i = 0; i < n_; ++i) th_.emplace_back([this, i] { run(i); });
 }
@@ -219,7 +222,7 @@ CopyPool::~CopyPool() {
     for (auto& t : th_) t.join();
 }
 
-void CopyPool::start(void* dst, const void* src, std::size_t bytes) {
+void CopyPool::start(void* dst, const void* src, std::size_t bytes, int streaming) {
     if (bytes <= kInlineBytes) {  // waking the pool costs more than the copy
         std::memcpy(dst, src, bytes);
         std::lock_guard<std::mutex> l(m_);
@@ -231,6 +234,7 @@ void CopyPool::start(void* dst, const void* src, std::size_t bytes) {
         dst_ = static_cast<char*>(dst);
         src_ = static_cast<const char*>(src);
         bytes_ = bytes;
+        job_nt_ = streaming < 0 ? nt_ : (streaming > 0 && nt_allowed_);
         left_ = n_;
         ++gen_;
     }
@@ -249,6 +253,7 @@ void CopyPool::run(int i) {
         char* d;
         const char* s;
         std::size_t b;
+        bool nt;
         {
             std::unique_lock<std::mutex> l(m_);
             cv_.wait(l, [&] { return stop_ || gen_ != seen; });
@@ -257,11 +262,12 @@ void CopyPool::run(int i) {
             d = dst_;
             s = src_;
             b = bytes_;
+            nt = job_nt_;
         }
         // piece i of n_, page-aligned so that threads never share a page
         const std::size_t per = ((b + n_ - 1) / n_ + 4095) & ~std::size_t(4095);
         const std::size_t lo = std::min(b, per * std::size_t(i)), hi = std::min(b, lo + per);
-        if (hi > lo) stream_copy(d + lo, s + lo, hi - lo, nt_);
+        if (hi > lo) stream_copy(d + lo, s + lo, hi - lo, nt);
         {
             std::lock_guard<std::mutex> l(m_);
             if (--left_ == 0) done_cv_.notify_all();

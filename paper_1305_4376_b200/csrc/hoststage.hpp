@@ -76,7 +76,9 @@ public:
     CopyPool& operator=(const CopyPool&) = delete;
     // copies of at most kInlineBytes run on the calling thread
     static constexpr std::size_t kInlineBytes = std::size_t(64) << 10;
-    void start(void* dst, const void* src, std::size_t bytes);
+    // streaming: 1 / 0 = this job with / without streaming stores, -1 = the
+    // pool's default
+    void start(void* dst, const void* src, std::size_t bytes, int streaming = -1);
     void wait();
     int threads() const { return n_; }
 
@@ -84,7 +86,9 @@ private:
     void run(int i);
     const int n_;
     const NumaNode node_;
-    const bool nt_;
+    const bool nt_allowed_;  // T3DES_HOST_NT_COPY (experiments) can switch streaming stores off
+    const bool nt_;          // the default for jobs
+    bool job_nt_ = false;
     std::mutex m_;
     std::condition_variable cv_, done_cv_;
     std::uint64_t gen_ = 0;

@@ -28,11 +28,14 @@ for mib in (16, 64, 128, 256, 512, 1024):
     out[mib] = n / statistics.median(v) / 1e9
 print(json.dumps(out))
 '''
-res = {"0": {}, "1": {}}
+res = {"0": {}, "1": {}, "default": {}}
 for r in range(3):
-    for nt in ("0", "1"):
-        p = subprocess.run([sys.executable, "-c", CHILD, ROOT], capture_output=True, text=True, timeout=600,
-                           env=dict(os.environ, T3DES_HOST_NT_IN=nt))
+    for nt in ("0", "1", "default"):
+        env = dict(os.environ)
+        env.pop("T3DES_HOST_NT_IN", None)
+        if nt != "default":
+            env["T3DES_HOST_NT_IN"] = nt
+        p = subprocess.run([sys.executable, "-c", CHILD, ROOT], capture_output=True, text=True, timeout=600, env=env)
         if p.returncode:
             print(nt, p.stderr[-300:])
             continue
