@@ -51,6 +51,17 @@ using t3b::DeviceScope;
 
 using t3b::partial_overlap;
 
+// Test hook (tests/test_gpu_parity.py::test_host_pipeline_error_leaves_no_copy_in_flight):
+// T3DES_FAULT_AT_STAGE=k makes stage k of the host pipelines fail as a launch
+// would, so the error paths' "no copy in flight after return" can be tested.
+bool fault_at(std::size_t stage) {
+    static const long k = [] {
+        const char* e = std::getenv("T3DES_FAULT_AT_STAGE");
+        return e ? std::atol(e) : -1L;
+    }();
+    return k >= 0 && stage == static_cast<std::size_t>(k);
+}
+
 int launch_sptable(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8_t* out,
                    std::uint64_t nblocks, cudaStream_t s);
 
@@ -448,7 +459,7 @@ int ecb_host_staged(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8
             if (!rc) rc = launch_sptable(c, dir, static_cast<std::uint8_t*>(d), static_cast<std::uint8_t*>(d), n / 8, s);
         } else {
             if (cudaMemcpyAsync(c->hdev[slot], src, n, cudaMemcpyHostToDevice, s) != cudaSuccess) rc = T3DES_CU_ERR_CUDA;
-            if (!rc) rc = run_device(c, dir, c->hdev[slot], c->hdev[slot], n / 8, s);
+            if (!rc) rc = fault_at(k) ? T3DES_CU_ERR_CUDA : run_device(c, dir, c->hdev[slot], c->hdev[slot], n / 8, s);
             if (!rc && cudaMemcpyAsync(dst, c->hdev[slot], n, cudaMemcpyDeviceToHost, s) != cudaSuccess)
                 rc = T3DES_CU_ERR_CUDA;
         }
@@ -796,7 +807,7 @@ int t3des_cu_ecb_host(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uin
         cudaStream_t s = c->st[k % ns];
         std::uint8_t* b = c->buf[k % ns];
         if (cudaMemcpyAsync(b, in + off, n, cudaMemcpyHostToDevice, s) != cudaSuccess) rc = T3DES_CU_ERR_CUDA;
-        if (!rc) rc = run_device(c, dir, b, b, n / 8, s);
+        if (!rc) rc = fault_at(k) ? T3DES_CU_ERR_CUDA : run_device(c, dir, b, b, n / 8, s);
         if (!rc && cudaMemcpyAsync(out + off, b, n, cudaMemcpyDeviceToHost, s) != cudaSuccess) rc = T3DES_CU_ERR_CUDA;
     }
     for (int i = 0; i < ns; ++i)

@@ -7,6 +7,7 @@ import ctypes
 import hashlib
 import os
 import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -654,6 +655,44 @@ def test_batch_api_from_several_threads(oracle):
     for t in th:
         t.join()
     assert not errors, errors
+
+
+FAULT_CHILD = r'''
+import sys, time
+sys.path.insert(0, sys.argv[1])
+import numpy as np, torch
+import paper_1305_4376_b200 as t3
+from paper_1305_4376_b200 import _native as N
+e = t3.Engine(0)
+e.set_schedule(t3.triple_schedule(t3.parse_hex_key("133457799BBCDFF10E329232EA6D0D737CA110454A1A6E57")))
+n = 512 << 20
+for kind in ("pinned", "pageable"):
+    if kind == "pinned":
+        src = torch.empty(n, dtype=torch.uint8).pin_memory(); dst = torch.empty(n, dtype=torch.uint8).pin_memory()
+        ps, pd = src.data_ptr(), dst.data_ptr(); view = dst.numpy()
+    else:
+        src = np.zeros(n, np.uint8); dst = np.zeros(n, np.uint8); ps, pd = src.ctypes.data, dst.ctypes.data; view = dst
+    view[:] = 0x5A
+    rc = N.lib().t3des_cu_ecb_host(e._h, 0, ps, pd, n)
+    assert rc == N.ERR_CUDA, (kind, rc)
+    snap = view.copy()
+    time.sleep(0.3)  # any copy still in flight would land now
+    assert np.array_equal(view, snap), kind + ": output changed after the call returned"
+    assert (view[-(1 << 20):] == 0x5A).all(), kind + ": stages after the failing one were written"
+print("ok")
+'''
+
+
+def test_host_pipeline_error_leaves_no_copy_in_flight():
+    """A failing stage in the host pipelines (pinned DMA pipeline, pageable
+    staging) returns an error only after every queued copy has finished: the
+    caller's output does not change after the call returns (ADVICE r1), and
+    later stages are never written.  T3DES_FAULT_AT_STAGE injects the failure
+    at stage 3 (a fresh process: the hook is read once)."""
+    env = dict(os.environ, T3DES_FAULT_AT_STAGE="3")
+    p = subprocess.run([sys.executable, "-c", FAULT_CHILD, ROOT], capture_output=True, text=True, env=env,
+                       timeout=300)
+    assert p.returncode == 0 and p.stdout.strip().endswith("ok"), p.stdout + p.stderr
 
 
 def test_auto_variant_with_large_work_group(eng, oracle):
