@@ -674,7 +674,9 @@ for kind in ("pinned", "pageable"):
         src = np.zeros(n, np.uint8); dst = np.zeros(n, np.uint8); ps, pd = src.ctypes.data, dst.ctypes.data; view = dst
     view[:] = 0x5A
     rc = N.lib().t3des_cu_ecb_host(e._h, 0, ps, pd, n)
+    head = view[:1 << 20].copy()  # read at once: the stages before the failing one must already be out
     assert rc == N.ERR_CUDA, (kind, rc)
+    assert not (head == 0x5A).any(), kind + ": an earlier stage had not landed when the call returned"
     snap = view.copy()
     time.sleep(0.3)  # any copy still in flight would land now
     assert np.array_equal(view, snap), kind + ": output changed after the call returned"
