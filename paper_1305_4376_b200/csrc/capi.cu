@@ -51,16 +51,7 @@ using t3b::DeviceScope;
 
 using t3b::partial_overlap;
 
-// Test hook (tests/test_gpu_parity.py::test_host_pipeline_error_leaves_no_copy_in_flight):
-// T3DES_FAULT_AT_STAGE=k makes stage k of the host pipelines fail as a launch
-// would, so the error paths' "no copy in flight after return" can be tested.
-bool fault_at(std::size_t stage) {
-    static const long k = [] {
-        const char* e = std::getenv("T3DES_FAULT_AT_STAGE");
-        return e ? std::atol(e) : -1L;
-    }();
-    return k >= 0 && stage == static_cast<std::size_t>(k);
-}
+using t3b::fault_at;
 
 int launch_sptable(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8_t* out,
                    std::uint64_t nblocks, cudaStream_t s);
@@ -262,6 +253,14 @@ std::size_t small_batch_stage(std::size_t len) {
 }  // namespace
 
 namespace t3b {
+
+bool fault_at(std::size_t stage) {
+    static const long k = [] {
+        const char* e = std::getenv("T3DES_FAULT_AT_STAGE");
+        return e ? std::atol(e) : -1L;
+    }();
+    return k >= 0 && stage == static_cast<std::size_t>(k);
+}
 
 int run_device(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8_t* out, std::uint64_t nblocks,
                cudaStream_t s) {

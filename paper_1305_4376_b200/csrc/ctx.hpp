@@ -97,6 +97,11 @@ inline bool partial_overlap(const void* a, const void* b, std::size_t len) {
 // host copy threads of the pageable staging path (in + out pools)
 constexpr int kMaxCopyThreads = 14;
 
+// Test hook: T3DES_FAULT_AT_STAGE=k makes stage (chunk) k of the host
+// pipelines and the stream path fail as a launch would, so their error paths
+// can be tested (tests/test_gpu_parity.py, tests/test_streams.py).
+bool fault_at(std::size_t stage);
+
 // Transform nblocks device blocks on stream s (in may equal out), honouring
 // the context's variant and launch shaping.  Returns a T3DES_CU_* status.
 int run_device(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8_t* out, std::uint64_t nblocks,

@@ -206,7 +206,7 @@ StreamStats run_stream(t3des_cu_ctx* c, int dir, ByteSource& src, ByteSink& dst,
             std::uint8_t* d = c->buf[slot];
             int rc = cudaMemcpyAsync(d, ring.p[slot], n, cudaMemcpyHostToDevice, s) == cudaSuccess ? 0
                                                                                                   : T3DES_CU_ERR_CUDA;
-            if (!rc) rc = run_device(c, dir, d, d, n / 8, s);
+            if (!rc) rc = fault_at(std::size_t(k)) ? T3DES_CU_ERR_CUDA : run_device(c, dir, d, d, n / 8, s);
             if (!rc && cudaMemcpyAsync(ring.p[slot], d, n, cudaMemcpyDeviceToHost, s) != cudaSuccess)
                 rc = T3DES_CU_ERR_CUDA;
             if (rc) {

@@ -5,6 +5,7 @@ t3des_cu_stream_fd) and through the C++ mirror (istream/ostream)."""
 import io
 import os
 import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -317,3 +318,37 @@ def test_streams_match_reference_outputs_and_errors(tmp_path, via):
         assert len(got) == c["written_len"] and hashlib.sha256(got).hexdigest() == c["written_sha256"], name
         if err == "none":
             assert (rep.bytes_in, rep.bytes_out, rep.chunks) == (c["bytes_in"], c["bytes_out"], c["chunks"]), name
+
+
+STREAM_FAULT_CHILD = r'''
+import io, sys
+sys.path.insert(0, sys.argv[1])
+import numpy as np
+import paper_1305_4376_b200 as t3
+from tests.oracle_util import Oracle
+o = Oracle.load()
+key = "0123456789ABCDEF23456789ABCDEF01456789ABCDEF0123"
+ts = t3.triple_schedule(t3.parse_hex_key(key))
+cb = 16
+body = np.random.default_rng(53).integers(0, 256, 8 * cb * 10, dtype=np.uint8)
+out = io.BytesIO()
+try:
+    t3.encrypt_stream(io.BytesIO(body.tobytes()), out, ts, t3.DispatchConfig(chunk_blocks=cb), t3.PaddingMode.NONE)
+    raise SystemExit("no error")
+except t3.CudaError:
+    pass
+want = o.ecb(body[: 8 * cb * 3], o.schedule_hex(key), 0).tobytes()
+assert out.getvalue() == want, (len(out.getvalue()), len(want))
+print("ok")
+'''
+
+
+@pytest.mark.gpu
+def test_stream_gpu_failure_writes_the_chunks_before_it():
+    """A GPU failure at chunk 3 of a stream (fault injection,
+    T3DES_FAULT_AT_STAGE) surfaces as CudaError after the three earlier
+    chunks have been written, like the reference's stream errors."""
+    env = dict(os.environ, T3DES_FAULT_AT_STAGE="3")
+    p = subprocess.run([sys.executable, "-c", STREAM_FAULT_CHILD, ROOT], capture_output=True, text=True, env=env,
+                       timeout=300)
+    assert p.returncode == 0 and p.stdout.strip().endswith("ok"), p.stdout + p.stderr
