@@ -358,8 +358,10 @@ int ecb_host_staged(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8
         // thread).  Copies into the pinned slots choose per batch (below).
         // Overrides for experiments: T3DES_HOST_NT_IN / T3DES_HOST_NT_OUT.
         auto flag = [](const char* n, bool d) { const char* e = std::getenv(n); return e ? std::atoi(e) != 0 : d; };
-        c->pool_in = new t3b::CopyPool((total + 1) / 2, node, flag("T3DES_HOST_NT_IN", true));
-        c->pool_out = new t3b::CopyPool(std::max(1, total / 2), node, flag("T3DES_HOST_NT_OUT", true));
+        int nin = (total + 1) / 2;
+        if (const char* e = std::getenv("T3DES_HOST_IN_THREADS")) nin = std::clamp(std::atoi(e), 1, total - 1);  // experiments
+        c->pool_in = new t3b::CopyPool(nin, node, flag("T3DES_HOST_NT_IN", true));
+        c->pool_out = new t3b::CopyPool(std::max(1, total - nin), node, flag("T3DES_HOST_NT_OUT", true));
     }
     const std::size_t nst = (len + S - 1) / S;
     // One small stage between two pageable spans: copy in, run the SP-table
