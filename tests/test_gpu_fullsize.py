@@ -174,6 +174,10 @@ def test_configs3_64gib_whole_output_and_shard_edges(eng, oracle):
         first, count = shard_range(n, 8, r)
         k0, k1 = first >> 27, (first + count) >> 27
         assert eng.checksum(buf.data_ptr() + 8 * first, first, count, st) == sum(pieces[k0:k1]) % 2**64
+    # and the whole 64 GiB ciphertext decrypts (one launch, in place) to the
+    # reference's plaintext checksum
+    eng.ecb_device(1, buf.data_ptr(), buf.data_ptr(), 8 * n, st)
+    assert eng.checksum(buf.data_ptr(), 0, n, st) == int(gold["plaintext_checksum"], 16)
 
 
 def _enc_dev(e, hexkey, x_dev, direction=0):
