@@ -499,8 +499,39 @@ def extra_configs(e, t3, N, torch, np) -> dict:
                                       "kat_3FA40E8A984D4815": kat.hex().upper() == "3FA40E8A984D4815",
                                       "round_trip_ok": bool(torch.equal(b1, b2)),
                                       "note": "K1 = K2 = K3: EDE collapses to single DES, 16 rounds"}
-    del b1, b2
+    del b2
     e3.close()
+    # the key-specialised variant (NVRTC at run time, opt-in):
+    # compile + load time, then the configs[1] payload through it, checked
+    # against the shipped kernel's output
+    e.set_variant(N.VARIANT_KEYED)
+    try:
+        t_first = e.keyed_prepare(0)
+        t_hit = e.keyed_prepare(0)
+        e.fill_splitmix(b1.data_ptr(), 0, n1, SEED, stream)
+        kb = torch.empty_like(b1)
+        e.ecb_device(0, b1.data_ptr(), kb.data_ptr(), 8 * n1, stream)
+        torch.cuda.synchronize()
+        ev0.record()
+        for _ in range(5):
+            e.ecb_device(0, b1.data_ptr(), kb.data_ptr(), 8 * n1, stream)
+        ev1.record()
+        torch.cuda.synchronize()
+        msk = ev0.elapsed_time(ev1) / 5
+        e.set_variant(N.VARIANT_AUTO)
+        ref = torch.empty_like(b1)
+        e.ecb_device(0, b1.data_ptr(), ref.data_ptr(), 8 * n1, stream)
+        torch.cuda.synchronize()
+        out["f4_keyed_1GiB_encrypt"] = {
+            "device_GBps": round(8 * n1 / msk / 1e6, 2), "jit_compile_load_s": round(t_first, 3),
+            "cache_hit_s": round(t_hit, 6), "equal_to_shipped_kernel": bool(torch.equal(kb, ref)),
+            "note": "T3DES_CU_VARIANT_KEYED: round keys folded into LOP3 immediates, NVRTC-compiled for this key; "
+                    "opt-in, AUTO keeps the table-driven kernel (same ALU work per block, DESIGN §3.7)"}
+        del kb, ref
+    except Exception as exc:  # NVRTC missing on the box: report, never a fallback
+        out["f4_keyed_1GiB_encrypt"] = {"unavailable": f"{type(exc).__name__}: {exc}"}
+    e.set_variant(N.VARIANT_BITSLICE)
+    del b1
     torch.cuda.empty_cache()
     # configs[3]: the 64 GiB stream on one device — one launch, and the 8
     # block ranges 8 GPUs would own run back to back — checked against the
@@ -596,7 +627,8 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--variant", choices=["bitslice", "bitslice_alu", "bitslice_dfma", "bitslice_shrfma", "bitslice_ldg", "sptable"], default="bitslice")
+    ap.add_argument("--variant", choices=["bitslice", "bitslice_alu", "bitslice_dfma", "bitslice_shrfma", "bitslice_ldg", "sptable",
+                                          "keyed"], default="bitslice")
     ap.add_argument("--gib", type=int, default=1, help="GiB per step at N = 1 (configs[1])")
     ap.add_argument("--c3-gib", type=int, default=64, help="global GiB per step at N > 1 (configs[3])")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -687,7 +719,7 @@ def main() -> None:
     e.set_schedule(ts)
     VARIANTS = {"bitslice": N.VARIANT_BITSLICE, "bitslice_alu": N.VARIANT_BITSLICE_ALU,
                 "bitslice_dfma": N.VARIANT_BITSLICE_DFMA, "bitslice_shrfma": N.VARIANT_BITSLICE_SHRFMA,
-                "bitslice_ldg": N.VARIANT_BITSLICE_LDG, "sptable": N.VARIANT_SPTABLE}
+                "bitslice_ldg": N.VARIANT_BITSLICE_LDG, "sptable": N.VARIANT_SPTABLE, "keyed": N.VARIANT_KEYED}
     e.set_variant(VARIANTS[args.variant])
     from paper_1305_4376_b200.sharding import shard_range
 

@@ -44,6 +44,7 @@ extern "C" {
 #define T3DES_CU_ERR_NO_SCHEDULE 7 /* t3des_cu_set_schedule not called yet  */
 #define T3DES_CU_ERR_PADDING 8     /* malformed PKCS#7 padding (PaddingError) */
 #define T3DES_CU_ERR_IO 9          /* stream read/write failure (IoError)    */
+#define T3DES_CU_ERR_JIT 10        /* NVRTC missing or the keyed compile failed */
 
 #define T3DES_CU_ENCRYPT 0
 #define T3DES_CU_DECRYPT 1
@@ -60,6 +61,17 @@ extern "C" {
  * of one warp per 1024 blocks; measured crossover ~1 MiB). */
 #define T3DES_CU_VARIANT_AUTO 6
 #define T3DES_CU_AUTO_SMALL_BLOCKS 131072
+/* Key-specialised bitsliced kernel: the installed schedule's
+ * round keys folded into the LOP3 immediates of a cipher that NVRTC compiles
+ * at run time, one module per (key sequence, direction), kept for the
+ * process lifetime.  Opt-in, never chosen by AUTO: it executes the same ALU
+ * operations per block as the table-driven kernel (whitening already keeps
+ * the key XORs off the ALU pipe), and the first use of a key
+ * pays the compile (t3des_cu_keyed_prepare; seconds).  Full 1024-block tiles
+ * of 16-byte aligned spans run keyed; a partial tile and unaligned spans run
+ * the table-driven kernels.  The compiled code embeds the key: it is held in
+ * process and device memory only, never written to disk. */
+#define T3DES_CU_VARIANT_KEYED 7
 
 typedef struct t3des_cu_ctx t3des_cu_ctx;
 
@@ -94,6 +106,21 @@ int t3des_cu_set_schedule(t3des_cu_ctx* ctx, const uint64_t sub48[48]);
 
 /* T3DES_CU_VARIANT_*; default AUTO. */
 int t3des_cu_set_variant(t3des_cu_ctx* ctx, int variant);
+
+/* T3DES_CU_VARIANT_KEYED: compile (or find in the process cache) the keyed
+ * kernel for the installed schedule and `direction` and load it on the
+ * context's device, so that no later launch pays for it (call it before
+ * capturing a CUDA graph).  *compile_seconds (may be NULL) = the time spent
+ * here, 0 on a cache hit.  T3DES_CU_ERR_JIT when NVRTC is unavailable
+ * (libnvrtc.so.12; T3DES_NVRTC names another path) or fails. */
+int t3des_cu_keyed_prepare(t3des_cu_ctx* ctx, int direction, double* compile_seconds);
+
+/* Context-free and device-free: the keyed kernel's CUBIN (sm_100a) for a
+ * schedule and direction, as t3des_cu_keyed_prepare builds it — for
+ * inspection and tests (no GPU needed).  *size = the CUBIN's size; the bytes
+ * are written when capacity >= *size (cubin may be NULL to query). */
+int t3des_cu_keyed_compile(const uint64_t sub48[48], int direction, void* cubin, size_t capacity, size_t* size,
+                           double* compile_seconds);
 
 /* Launch shaping, the GPU reading of DispatchConfig (dispatch.hpp:25-30):
  * chunk_blocks = blocks per kernel launch (0 = whole batch in one launch,

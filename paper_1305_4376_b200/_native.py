@@ -24,6 +24,7 @@ ERR_CUDA = 6
 ERR_NO_SCHEDULE = 7
 ERR_PADDING = 8
 ERR_IO = 9
+ERR_JIT = 10
 
 ENCRYPT = 0
 DECRYPT = 1
@@ -34,6 +35,7 @@ VARIANT_BITSLICE_ALU = 3
 VARIANT_BITSLICE_DFMA = 4
 VARIANT_BITSLICE_SHRFMA = 5
 VARIANT_AUTO = 6
+VARIANT_KEYED = 7  # key-specialised, NVRTC-compiled at run time (opt-in)
 AUTO_SMALL_BLOCKS = 131072
 MULTI_STAGE_ALL = 1  # t3des_cu_ecb_multi_device flags
 MULTI_COPY = 2
@@ -61,6 +63,8 @@ SIGNATURES = {
     "t3des_cu_destroy": (_i, [_vp]),
     "t3des_cu_set_schedule": (_i, [_vp, _u64p]),
     "t3des_cu_set_variant": (_i, [_vp, _i]),
+    "t3des_cu_keyed_prepare": (_i, [_vp, _i, ctypes.POINTER(ctypes.c_double)]),
+    "t3des_cu_keyed_compile": (_i, [_u64p, _i, _vp, _sz, ctypes.POINTER(_sz), ctypes.POINTER(ctypes.c_double)]),
     "t3des_cu_set_launch": (_i, [_vp, _sz, _i]),
     "t3des_cu_ecb_device": (_i, [_vp, _i, _vp, _vp, _sz, _vp]),
     "t3des_cu_ecb_host": (_i, [_vp, _i, _vp, _vp, _sz]),

@@ -223,6 +223,14 @@ class Engine:
         _raise(self._lib.t3des_cu_set_variant(self._h, int(variant)))
         self._variant = int(variant)
 
+    def keyed_prepare(self, direction: int) -> float:
+        """VARIANT_KEYED: compile (or find cached) and load the key-specialised
+        kernel of the installed schedule for `direction`; returns the seconds
+        spent (0.0 on a cache hit)."""
+        secs = ctypes.c_double()
+        _raise(self._lib.t3des_cu_keyed_prepare(self._h, int(direction), ctypes.byref(secs)))
+        return secs.value
+
     def set_launch(self, chunk_blocks: int = 0, work_group: int = 0) -> None:
         shape = (int(chunk_blocks), int(work_group))
         if shape == self._launch:

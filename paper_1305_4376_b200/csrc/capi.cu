@@ -63,7 +63,8 @@ int launch_bitslice(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8
     // AUTO: the partial last tile (< 1024 blocks) runs on the SP-table kernel
     // (one thread per block, ~10 us instead of ~18 us for a 1-warp bitsliced
     // tile) on a side stream, concurrently with the full tiles.
-    const bool side_tail = tail && full && c->variant == T3DES_CU_VARIANT_AUTO;
+    const bool side_tail =
+        tail && full && (c->variant == T3DES_CU_VARIANT_AUTO || c->variant == T3DES_CU_VARIANT_KEYED);
     if (side_tail) {
         const std::uint64_t t0 = full * T3_TILE_BLOCKS;
         T3_CK(cudaEventRecord(c->ev_fork, s));
@@ -93,26 +94,17 @@ int launch_bitslice(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8
                             reinterpret_cast<std::uintptr_t>(out)) & 15u) == 0;
         const bool tma = vec4 && threads == T3_BS_THREADS && c->variant != T3DES_CU_VARIANT_BITSLICE_LDG;
         // tuning variants (A/B measurement of the T3_OPT_* code-generation options)
-        const int opt = (c->variant == T3DES_CU_VARIANT_BITSLICE || c->variant == T3DES_CU_VARIANT_AUTO) ? c->bs_opt
+        const int opt = (c->variant == T3DES_CU_VARIANT_BITSLICE || c->variant == T3DES_CU_VARIANT_AUTO ||
+                         c->variant == T3DES_CU_VARIANT_KEYED)
+                            ? c->bs_opt
                         : c->variant == T3DES_CU_VARIANT_BITSLICE_ALU ? 0
                         : c->variant == T3DES_CU_VARIANT_BITSLICE_DFMA ? T3_OPT_DFMA
                                                                        : T3_OPT_SHRFMA;
-#ifdef T3_KEYED_EXPERIMENT
-        if (tma && c->variant == T3DES_CU_VARIANT_BITSLICE) {
-            const int kthreads = T3_KEYED_WARPS * 32;
-            const int smem = T3_KEYED_WARPS * T3_TILE_BLOCKS * 8;
-            static bool attr = false;
-            if (!attr) {
-                T3_CK(cudaFuncSetAttribute(t3_bs_keyed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-                attr = true;
-            }
-            std::uint64_t kgrid = 148;
-            if (const char* e = std::getenv("T3_KEYED_GRID")) kgrid = std::strtoull(e, nullptr, 10);
-            t3_bs_keyed_kernel<<<unsigned(kgrid), kthreads, smem, s>>>(in, out, full);
-            return 0;
-        }
-#endif
-        if (tma && c->rounds == 16 && opt == T3_OPT_DEFAULT_VALUE) {
+        if (c->variant == T3DES_CU_VARIANT_KEYED && vec4) {
+            // key-specialised kernel (NVRTC, keyed.cpp); compiled on the first
+            // launch of a key unless t3des_cu_keyed_prepare ran
+            if (int rc = t3b::keyed_launch(c, dir, in, out, full, s)) return rc;
+        } else if (tma && c->rounds == 16 && opt == T3_OPT_DEFAULT_VALUE) {
             // collapsed EDE (K1 = K2 or K2 = K3): single DES, a third of the work
             t3_bs_tma_kernel<T3_OPT_DEFAULT_VALUE, 16>
                 <<<unsigned(grid), threads, 0, s>>>(in, out, full, c->bs16[dir]);
@@ -502,6 +494,7 @@ const char* t3des_cu_strerror(int code) {
         case T3DES_CU_ERR_NO_SCHEDULE: return "no key schedule installed";
         case T3DES_CU_ERR_PADDING: return "malformed PKCS#7 padding";
         case T3DES_CU_ERR_IO: return "stream read/write failure";
+        case T3DES_CU_ERR_JIT: return "keyed kernel: NVRTC unavailable or compilation failed";
         default: return "unknown error";
     }
 }
@@ -658,6 +651,7 @@ int t3des_cu_set_schedule(t3des_cu_ctx* c, const std::uint64_t sub48[48]) {
     // call): nothing to rebuild, and no device synchronisation
     if (c->have_schedule && std::memcmp(c->sub48, sub48, sizeof c->sub48) == 0) return T3DES_CU_OK;
     c->have_schedule = false;  // until every table below is rebuilt
+    c->keyed[0] = c->keyed[1] = nullptr;  // keyed modules are per key sequence
     c->rounds = 48;
     for (int dir = 0; dir < 2; ++dir) {
         std::uint64_t seq[48];
@@ -697,7 +691,7 @@ int t3des_cu_set_schedule(t3des_cu_ctx* c, const std::uint64_t sub48[48]) {
 }
 
 int t3des_cu_set_variant(t3des_cu_ctx* c, int variant) {
-    if (!c || variant < T3DES_CU_VARIANT_BITSLICE || variant > T3DES_CU_VARIANT_AUTO)
+    if (!c || variant < T3DES_CU_VARIANT_BITSLICE || variant > T3DES_CU_VARIANT_KEYED)
         return T3DES_CU_ERR_ARG;
     c->variant = variant;
     return T3DES_CU_OK;

@@ -66,6 +66,7 @@ struct t3des_cu_ctx {
     std::uint64_t launches = 0;
     cudaStream_t tail_st = nullptr;             // side stream for the partial tile (AUTO)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    const void* keyed[2] = {};  // VARIANT_KEYED: the schedule's loaded module per direction (keyed.cpp)
 };
 
 namespace t3b {
@@ -109,6 +110,13 @@ int run_device(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8_t* o
 
 // Make sure the first n staging buffers hold at least `bytes` each.
 int ensure_staging(t3des_cu_ctx* c, std::size_t bytes, int n);
+
+// VARIANT_KEYED (keyed.cpp): load the keyed module of c's schedule for `dir`
+// (compiling it on first use of that key sequence), and launch it over
+// `ntiles` full warp tiles of 16-byte aligned spans.
+int keyed_prepare(t3des_cu_ctx* c, int dir, double* seconds);
+int keyed_launch(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8_t* out, std::uint64_t ntiles,
+                 cudaStream_t s);
 
 // What a host-span pointer is, from one attribute query: device-only memory
 // (an error for the host entry points), page-locked host memory (DMA-able

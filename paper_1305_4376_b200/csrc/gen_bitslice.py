@@ -231,11 +231,6 @@ def gen_round(circuits) -> list[str]:
     return out
 
 
-def lut_flip_inputs(lut: int, flips: int) -> int:
-    """LUT of f(a ^ fa, b ^ fb, c ^ fc); flips bit 2/1/0 = a/b/c (minterm index order)."""
-    return sum(((lut >> (m ^ flips)) & 1) << m for m in range(8))
-
-
 def l_role(t: int) -> int:
     """0 if half A plays L in round t, else 1 (schedule.cpp build_bitslice_table)."""
     p, loc = divmod(t, 16)
@@ -243,45 +238,68 @@ def l_role(t: int) -> int:
     return 1 - a if p == 1 else a
 
 
-def gen_keyed_cipher(circuits, seq, name="t3_cipher_keyed", sync_every=0) -> list[str]:
-    """All len(seq) rounds unrolled with the round keys folded into the lop3
-    immediates: a key bit of 1 on an S-box input complements that input in
-    the LUT of every gate reading it.  No whitening, no key table, no FMA-pipe
-    corrections; Feistel tops merge for free (C no longer exists)."""
-    nrounds = len(seq)
+def gen_keyed_rounds(circuits) -> list[str]:
+    """The key-specialised round as a template on the 48-bit
+    round key K: the same circuits as gen_round, with each key bit folded into
+    the lop3 immediates of the gates reading that S-box input (a key bit of 1
+    complements the input: t3k_gate), so a round is the 186 S-box gates plus
+    the 32 Feistel lop3 and nothing else — no key table, no whitening, no
+    FMA-pipe corrections.  The immediates are constant expressions of K, so a
+    compiler (NVRTC at run time, csrc/keyed.cpp) instantiating
+    t3_keyed_round<K> for concrete keys emits plain LOP3s."""
     pos_to_p = {P[p]: p for p in range(32)}
-    out = [f"T3_FI void {name}(uint32_t (&A)[32], uint32_t (&B)[32]) {{"]
-    for t in range(nrounds):
-        lh = l_role(t) if nrounds == 48 else t % 2
-        L, R = ("A", "B") if lh == 0 else ("B", "A")
-        k = seq[t]
-        out.append(f"  {{  // round {t}: {L} ^= f({R})")
-        for box in range(8):
-            gates, outs = circuits[box]
-            names = {}
-            kinv = {}
-            for kvar in range(6):
-                j = 6 * box + 5 - kvar
-                names[kvar] = f"{R}[{E[j] - 1}]"
-                kinv[kvar] = (k >> (47 - j)) & 1
-            for g, a, b, c, lut in gates:
-                flips = (kinv.get(a, 0) << 2) | (kinv.get(b, 0) << 1) | kinv.get(c, 0)
-                out.append(f"    const uint32_t s{box}g{g} = lop3<0x{lut_flip_inputs(lut, flips):02x}>({names[a]}, {names[b]}, {names[c]});")
-                names[g] = f"s{box}g{g}"
-            for o in range(4):
-                p = pos_to_p[4 * box + 4 - o]
-                if outs[o][0] == "f":
-                    _, a, b, h = outs[o]
-                    fa, fb = kinv.get(a, 0), kinv.get(b, 0)
-                    h2 = sum(((h >> ((((q >> 1) ^ fa) << 1) | ((q & 1) ^ fb))) & 1) << q for q in range(4))
-                    out.append(f"    {L}[{p}] = lop3<0x{feistel_lut(h2):02x}>({L}[{p}], {names[a]}, {names[b]});")
-                else:
-                    g, inv = outs[o]
-                    inv ^= kinv.get(g, 0)  # an output read straight from an input
-                    out.append(f"    {L}[{p}] = lop3<0x{0x3c ^ (0xff if inv else 0):02x}>({L}[{p}], {names[g]}, 0u);")
-        out.append("  }")
-        if sync_every and (t + 1) % sync_every == 0 and t + 1 < nrounds:
-            out.append("  T3_KEYED_SYNC();")
+    out = [
+        "// key bit j (0-based FIPS subkey bit j+1, machine bit 47-j) of a round key; j < 0: none",
+        "T3K_CE unsigned t3k_bit(uint64_t K, int j) { return j < 0 ? 0u : unsigned((K >> (47 - j)) & 1u); }",
+        "// LUT of f(a ^ fa, b ^ fb, c ^ fc); fl bit 2/1/0 = fa/fb/fc",
+        "T3K_CE unsigned t3k_flip(unsigned lut, unsigned fl) {",
+        "    unsigned r = 0;",
+        "    for (unsigned m = 0; m < 8; ++m) r |= ((lut >> (m ^ fl)) & 1u) << m;",
+        "    return r;",
+        "}",
+        "T3K_CE unsigned t3k_gate(uint64_t K, unsigned lut, int ja, int jb, int jc) {",
+        "    return t3k_flip(lut, (t3k_bit(K, ja) << 2) | (t3k_bit(K, jb) << 1) | t3k_bit(K, jc));",
+        "}",
+        "// Feistel top: L ^ h(a ^ ka, b ^ kb) as one lop3 over (L, a, b)",
+        "T3K_CE unsigned t3k_ftop(uint64_t K, unsigned h, int ja, int jb) {",
+        "    const unsigned fa = t3k_bit(K, ja), fb = t3k_bit(K, jb);",
+        "    unsigned lut = 0;",
+        "    for (unsigned m = 0; m < 8; ++m) {",
+        "        const unsigned q = ((((m >> 1) & 1u) ^ fa) << 1) | ((m & 1u) ^ fb);",
+        "        lut |= (((m >> 2) & 1u) ^ ((h >> q) & 1u)) << m;",
+        "    }",
+        "    return lut;",
+        "}",
+        "// 0 if half A plays L in round t, else 1 (passes 0 and 2 start with A, pass 1",
+        "// with B: the pass swaps are role renaming, as in build_bitslice_table)",
+        f"constexpr int T3K_ROLE[48] = {{{', '.join(str(l_role(t)) for t in range(48))}}};",
+        "// L ^ (g ^ inv ^ kg): an output read from a gate (jg < 0) or an input",
+        "T3K_CE unsigned t3k_direct(uint64_t K, unsigned inv, int jg) { return 0x3cu ^ ((inv ^ t3k_bit(K, jg)) ? 0xffu : 0u); }",
+        "",
+        "// One round L ^= f(R, K) with K folded into the immediates.",
+        "template <uint64_t K>",
+        "T3_FI void t3_keyed_round(uint32_t (&L)[32], const uint32_t (&R)[32]) {",
+    ]
+    for box in range(8):
+        gates, outs = circuits[box]
+        names, kj = {}, {}
+        for kvar in range(6):
+            j = 6 * box + 5 - kvar
+            names[kvar] = f"R[{E[j] - 1}]"
+            kj[kvar] = j
+        out.append(f"    // S{box + 1}")
+        for g, a, b, c, lut in gates:
+            out.append(f"    const uint32_t s{box}g{g} = lop3<t3k_gate(K, 0x{lut:02x}, {kj.get(a, -1)}, {kj.get(b, -1)}, "
+                       f"{kj.get(c, -1)})>({names[a]}, {names[b]}, {names[c]});")
+            names[g] = f"s{box}g{g}"
+        for o in range(4):
+            p = pos_to_p[4 * box + 4 - o]
+            if outs[o][0] == "f":
+                _, a, b, h = outs[o]
+                out.append(f"    L[{p}] = lop3<t3k_ftop(K, 0x{h:x}, {kj.get(a, -1)}, {kj.get(b, -1)})>(L[{p}], {names[a]}, {names[b]});")
+            else:
+                g, inv = outs[o]
+                out.append(f"    L[{p}] = lop3<t3k_direct(K, {inv}, {kj.get(g, -1)})>(L[{p}], {names[g]}, 0u);")
     out.append("}")
     return out
 
@@ -357,6 +375,20 @@ def main() -> None:
     ]
     with open(os.path.join(gen_dir, "bitslice_tables.h"), "w") as f:
         f.write("\n".join(tab))
+    keyed = [
+        "// GENERATED by csrc/gen_bitslice.py from csrc/sbox_circuits/*.txt — do not edit.",
+        "// Key-specialised rounds (SURVEY §8f-4): included by keyed_kernel.cuh, which",
+        "// NVRTC compiles at run time for one key sequence (csrc/keyed.cpp).",
+        "#pragma once",
+        "#ifdef __CUDACC__",
+        "#define T3K_CE __host__ __device__ constexpr",
+        "#else",
+        "#define T3K_CE constexpr",
+        "#endif",
+        "",
+    ] + gen_keyed_rounds(circuits) + [""]
+    with open(os.path.join(gen_dir, "keyed_rounds.cuh"), "w") as f:
+        f.write("\n".join(keyed))
     print(f"generated: {total} lop3 over 8 S-boxes", file=sys.stderr)
 
 

@@ -22,6 +22,7 @@
 #include <stdint.h>
 
 #include "t3des_core.cuh"
+#include "tma.cuh"
 
 #ifndef T3_BS_THREADS
 #define T3_BS_THREADS 128  // CTA size of the bitsliced kernels
@@ -95,27 +96,6 @@ t3_bs_kernel(const uint8_t* in, uint8_t* out, uint64_t first_tile, uint64_t ntil
 // never stall the integer pipe (without it all warps of an SM reach their
 // loads in lockstep and the ALU idles ~10%, ncu profiles/r1).  Requires
 // 16-byte aligned in/out.
-__device__ __forceinline__ uint32_t t3_smem_addr(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void t3_tma_fetch(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                 "l"(src), "r"(bytes), "r"(bar)
-                 : "memory");
-}
-
-__device__ __forceinline__ void t3_mbar_wait(uint32_t bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "T3_WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra T3_WAIT_%=;\n}" ::"r"(bar),
-        "r"(parity)
-        : "memory");
-}
-
 template <int OPT, int ROUNDS = 48>
 __global__ void __launch_bounds__(T3_BS_THREADS, T3_BS_MIN_CTAS)
 t3_bs_tma_kernel(const uint8_t* in, uint8_t* out, uint64_t ntiles, const __grid_constant__ T3BsTable tab) {
@@ -160,57 +140,6 @@ t3_bs_tma_kernel(const uint8_t* in, uint8_t* out, uint64_t ntiles, const __grid_
             __stcs(dst + 32 * j, make_uint4(lo[2 * j], hi[2 * j], lo[2 * j + 1], hi[2 * j + 1]));
     }
 }
-
-#ifdef T3_KEYED_EXPERIMENT
-// Experiment: key-specialised cipher (scripts/gen_keyed.py), CTAs of
-// T3_KEYED_WARPS warps held in lockstep by __syncthreads inside the cipher so
-// that all warps of an SM fetch from one window of the ~180 KB unrolled code.
-// Every warp must run the same number of tiles (ntiles % (grid*warps) == 0).
-#ifndef T3_KEYED_WARPS
-#define T3_KEYED_WARPS 16
-#endif
-__global__ void __launch_bounds__(T3_KEYED_WARPS * 32, 1)
-t3_bs_keyed_kernel(const uint8_t* in, uint8_t* out, uint64_t ntiles) {
-    extern __shared__ __align__(128) uint4 kslot[];  // [T3_KEYED_WARPS][512]
-    __shared__ __align__(8) uint64_t bar[T3_KEYED_WARPS];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-    uint64_t tile = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const uint32_t sbar = t3_smem_addr(&bar[wib]);
-    const uint32_t sdst = t3_smem_addr(&kslot[wib * 512]);
-    if (lane == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar));
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        if (tile < ntiles) t3_tma_fetch(sdst, in + tile * (T3_TILE_BLOCKS * 8), T3_TILE_BLOCKS * 8, sbar);
-    }
-    __syncwarp();
-    uint32_t parity = 0;
-    for (; tile < ntiles; tile += nwarps) {
-        t3_mbar_wait(sbar, parity);
-        parity ^= 1u;
-        uint32_t lo[32], hi[32];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const uint4 v = kslot[wib * 512 + 32 * j + lane];
-            lo[2 * j] = v.x;
-            hi[2 * j] = v.y;
-            lo[2 * j + 1] = v.z;
-            hi[2 * j + 1] = v.w;
-        }
-        __syncwarp();
-        const uint64_t next = tile + nwarps;
-        if (lane == 0 && next < ntiles) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            t3_tma_fetch(sdst, in + next * (T3_TILE_BLOCKS * 8), T3_TILE_BLOCKS * 8, sbar);
-        }
-        t3_tile32_keyed(lo, hi);
-        uint4* dst = reinterpret_cast<uint4*>(out + tile * (T3_TILE_BLOCKS * 8)) + lane;
-#pragma unroll
-        for (int j = 0; j < 16; ++j)
-            __stcs(dst + 32 * j, make_uint4(lo[2 * j], hi[2 * j], lo[2 * j + 1], hi[2 * j + 1]));
-    }
-}
-#endif
 
 // ---- SP-table kernel ---------------------------------------------------
 __device__ __forceinline__ void t3_dswap(uint32_t& a, uint32_t& b, int s, uint32_t m) {

@@ -281,23 +281,3 @@ T3_FI void t3_tile32(uint32_t (&lo)[32], uint32_t (&hi)[32], const KP w) {
     t3_transpose32<OPT>(hi);
 }
 
-#ifdef T3_KEYED_EXPERIMENT
-#include "build/keyed.cuh"
-// Experiment (scripts/gen_keyed.py): the tile with a key-specialised cipher.
-T3_FI void t3_tile32_keyed(uint32_t (&lo)[32], uint32_t (&hi)[32]) {
-    t3_transpose32<0>(lo);
-    t3_transpose32<0>(hi);
-    uint32_t A[32] = T3_GATHER_A(lo, hi);
-    uint32_t B[32] = T3_GATHER_B(lo, hi);
-    t3_cipher_keyed(A, B);
-    uint32_t olo[32] = T3_SCATTER_LO(A, B);
-    uint32_t ohi[32] = T3_SCATTER_HI(A, B);
-#pragma unroll
-    for (int k = 0; k < 32; ++k) {
-        lo[k] = olo[k];
-        hi[k] = ohi[k];
-    }
-    t3_transpose32<0>(lo);
-    t3_transpose32<0>(hi);
-}
-#endif
