@@ -375,8 +375,25 @@ def main() -> None:
     ]
     with open(os.path.join(gen_dir, "bitslice_tables.h"), "w") as f:
         f.write("\n".join(tab))
+    # The keyed kernel has no whitening word C, so an output in Feistel-top
+    # form h(a, b) merges into the Feistel lop3 for free: circuits searched
+    # with free tops (tools/sboxgen SBOXGEN_FEISTEL=1 SBOXGEN_TOP_COST=0) that
+    # are smaller by that measure live in sbox_circuits_keyed/ and replace the
+    # shipped ones for the keyed rounds only.
+    kcirc, ktotal = [], 0
+    for box in range(8):
+        path = os.path.join(HERE, "sbox_circuits_keyed", f"box{box}.txt")
+        if os.path.exists(path) and os.environ.get("T3_GEN_KEYED_BASE") != "1":  # (A/B: shipped circuits)
+            gates, outs = load_circuit(box, path)
+            verify_circuit(box, gates, outs)
+        else:
+            gates, outs = circuits[box]
+        kcirc.append((gates, outs))
+        ktotal += len(gates)
     keyed = [
-        "// GENERATED by csrc/gen_bitslice.py from csrc/sbox_circuits/*.txt — do not edit.",
+        "// GENERATED by csrc/gen_bitslice.py from csrc/sbox_circuits/*.txt and",
+        "// csrc/sbox_circuits_keyed/*.txt — do not edit.",
+        f"// {ktotal} S-box gates per round (Feistel tops merged into the 32 Feistel lop3).",
         "// Key-specialised rounds (SURVEY §8f-4): included by keyed_kernel.cuh, which",
         "// NVRTC compiles at run time for one key sequence (csrc/keyed.cpp).",
         "#pragma once",
@@ -386,7 +403,7 @@ def main() -> None:
         "#define T3K_CE constexpr",
         "#endif",
         "",
-    ] + gen_keyed_rounds(circuits) + [""]
+    ] + gen_keyed_rounds(kcirc) + [""]
     with open(os.path.join(gen_dir, "keyed_rounds.cuh"), "w") as f:
         f.write("\n".join(keyed))
     print(f"generated: {total} lop3 over 8 S-boxes", file=sys.stderr)

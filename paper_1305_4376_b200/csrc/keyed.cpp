@@ -107,8 +107,19 @@ int compile_cubin(const std::uint64_t* seq, int rounds, std::vector<char>& cubin
         NVRTC_SUCCESS)
         rc = T3DES_CU_ERR_JIT;
     if (!rc) {
-        const char* opts[] = {"-arch=sm_100a", "-std=c++17", "-lineinfo", "-DT3_NVRTC=1"};
-        const nvrtcResult cr = nv.compile(prog, int(sizeof opts / sizeof opts[0]), opts);
+        std::vector<const char*> opts = {"-arch=sm_100a", "-std=c++17", "-lineinfo", "-DT3_NVRTC=1"};
+        // experiments: extra NVRTC options, e.g. "-DT3_KEYED_SYNC_EVERY=8"
+        std::vector<std::string> extra;
+        if (const char* e = std::getenv("T3DES_KEYED_NVRTC_OPTS")) {
+            std::string all(e);
+            for (std::size_t p = 0; p < all.size();) {
+                const std::size_t q = std::min(all.find(' ', p), all.size());
+                if (q > p) extra.push_back(all.substr(p, q - p));
+                p = q + 1;
+            }
+        }
+        for (const auto& x : extra) opts.push_back(x.c_str());
+        const nvrtcResult cr = nv.compile(prog, int(opts.size()), opts.data());
         if (cr != NVRTC_SUCCESS || std::getenv("T3DES_JIT_VERBOSE")) {
             std::size_t n = 0;
             if (nv.log_size(prog, &n) == NVRTC_SUCCESS && n > 1) {

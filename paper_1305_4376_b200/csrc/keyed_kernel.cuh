@@ -16,8 +16,9 @@
 // CTA is therefore 16 warps, one per SM, held within T3_KEYED_SYNC_EVERY
 // rounds of each other by __syncthreads, so all warps of an SM fetch from
 // one window of the code.  Every warp of the grid runs the same number of
-// iterations (warps past the last tile compute on zeros and store nothing),
-// which keeps the barriers uniform for any tile count.
+// passes; a warp past the last tile computes on zeros and stores nothing,
+// which keeps the barriers uniform for any tile count (letting it take only
+// the barriers measured 3% slower, profiles/r2/keyed_ab_r2y.jsonl).
 //
 // Also compiles as plain host C++ (tests/native/keyed_host.cpp): the rounds
 // and tile function then run on the CPU for the parity tests.
@@ -30,7 +31,7 @@
 #define T3_KEYED_WARPS 16  // warps per CTA (one CTA per SM)
 #endif
 #ifndef T3_KEYED_SYNC_EVERY
-#define T3_KEYED_SYNC_EVERY 4  // rounds between CTA barriers (profiles/r1/keyed_experiment_r1g.txt)
+#define T3_KEYED_SYNC_EVERY 12  // rounds between CTA barriers (scripts/r2_keyed_ab2.sh: 8-16 best, >= 24 thrashes)
 #endif
 #ifdef __CUDA_ARCH__
 #define T3_KEYED_SYNC() __syncthreads()
@@ -90,7 +91,7 @@ t3_keyed_kernel(const uint8_t* in, uint8_t* out, uint64_t ntiles) {
     __syncwarp();
     uint32_t parity = 0;
     for (uint64_t it = 0; it < iters; ++it, tile += nwarps) {
-        const bool live = tile < ntiles;
+        const bool live = tile < ntiles;  // warp-uniform
         uint32_t lo[32], hi[32];
         if (live) {
             t3_mbar_wait(sbar, parity);
