@@ -99,7 +99,8 @@ struct DispatchConfig {
     unsigned workers = 0;               // CUDA: block-range shards round-robin over the GPUs from `device` (0 = 1)
     Backend backend = Backend::Cuda;
     int device = 0;                     // first CUDA device
-    int variant = 6;                    // T3DES_CU_VARIANT_*: 6 auto (default), 0 bitsliced, 1 SP-table
+    int variant = 6;                    // T3DES_CU_VARIANT_*: 6 auto (default), 0 bitsliced, 1 SP-table,
+                                        // 7 key-specialised (NVRTC at run time, opt-in)
     bool gpu_chunked = false;           // apply chunk_blocks/work_group to launches
 };
 

@@ -202,3 +202,31 @@ def test_keyed_module_cache_follows_the_schedule(keng, oracle):
         assert np.array_equal(got, oracle.ecb(x, oracle.schedule_hex(k), 0)), k
     keng.set_schedule(t3.triple_schedule(t3.parse_hex_key(ka)))
     assert keng.keyed_prepare(0) < 0.05
+
+
+@pytest.mark.gpu
+def test_keyed_variant_in_a_cuda_graph(keng, oracle):
+    """Prepared up front, the keyed kernel captures into a CUDA graph (the
+    C ABI is stream-ordered) and replays with the right output; the capture
+    itself compiles nothing."""
+    import paper_1305_4376_b200 as t3
+    from paper_1305_4376_b200 import _native as N
+
+    key = "0123456789ABCDEF23456789ABCDEF01456789ABCDEF0123"
+    keng.set_schedule(t3.triple_schedule(t3.parse_hex_key(key)))
+    keng.set_variant(N.VARIANT_KEYED)
+    keng.keyed_prepare(0)
+    keng.keyed_prepare(1)
+    x = oracle.splitmix(0, 1024 * 500 + 17, 21)
+    xd = torch.from_numpy(x).cuda()
+    y, z = torch.empty_like(xd), torch.empty_like(xd)
+    gs = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=gs):
+        keng.ecb_device(0, xd.data_ptr(), y.data_ptr(), xd.numel(), gs.cuda_stream)
+        keng.ecb_device(1, y.data_ptr(), z.data_ptr(), xd.numel(), gs.cuda_stream)
+    with torch.cuda.stream(gs):
+        g.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(y.cpu().numpy(), oracle.ecb(x, oracle.schedule_hex(key), 0))
+    assert torch.equal(z, xd)
