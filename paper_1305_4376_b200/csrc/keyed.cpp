@@ -230,7 +230,8 @@ int keyed_launch(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8_t*
     // number of tiles (keyed_kernel.cuh)
     const std::uint64_t grid =
         std::min<std::uint64_t>(std::uint64_t(c->sms), (ntiles + kKeyedWarps - 1) / kKeyedWarps);
-    void* args[] = {&in, &out, &ntiles};
+    std::uint32_t zero = 0;  // an operand the compiler cannot fold (T3_KEYED_PIN experiments)
+    void* args[] = {&in, &out, &ntiles, &zero};
     if (cudaLaunchKernel(reinterpret_cast<const void*>(m->kern), dim3(unsigned(std::max<std::uint64_t>(grid, 1))),
                          dim3(kKeyedWarps * 32), args, kKeyedSmem, s) != cudaSuccess) {
         (void)cudaGetLastError();

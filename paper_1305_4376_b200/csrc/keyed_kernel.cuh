@@ -13,12 +13,12 @@
 // The 48 unrolled rounds are ~180 KB of SASS, more than the instruction
 // caches hold, so warps that drift apart thrash them (measured: 3.26 ms/GiB
 // with free-running 4-warp CTAs, profiles/r1/keyed_experiment_r1g.txt).  A
-// CTA is therefore 16 warps, one per SM, held within T3_KEYED_SYNC_EVERY
-// rounds of each other by __syncthreads, so all warps of an SM fetch from
-// one window of the code.  Every warp of the grid runs the same number of
-// passes; a warp past the last tile computes on zeros and stores nothing,
-// which keeps the barriers uniform for any tile count (letting it take only
-// the barriers measured 3% slower, profiles/r2/keyed_ab_r2y.jsonl).
+// CTA is therefore 16 warps, one per SM, re-aligned by CTA barriers pinned at
+// the pass boundaries, so all warps of an SM fetch from one window of the
+// code.  Every warp of the grid runs the same number of passes; a warp past
+// the last tile computes on zeros and stores nothing, which keeps the
+// barriers uniform for any tile count (letting it take only the barriers
+// measured 3% slower, profiles/r2/keyed_ab_r2y.jsonl).
 //
 // Also compiles as plain host C++ (tests/native/keyed_host.cpp): the rounds
 // and tile function then run on the CPU for the parity tests.
@@ -30,34 +30,50 @@
 #ifndef T3_KEYED_WARPS
 #define T3_KEYED_WARPS 16  // warps per CTA (one CTA per SM)
 #endif
-#ifndef T3_KEYED_SYNC_EVERY
-#define T3_KEYED_SYNC_EVERY 12  // rounds between CTA barriers (scripts/r2_keyed_ab2.sh: 8-16 best, >= 24 thrashes)
-#endif
-#ifdef __CUDA_ARCH__
-#define T3_KEYED_SYNC() __syncthreads()
+// CTA barriers every T3K_SYNC rounds: at the pass boundaries (rounds 16 and
+// 32) of the 48-round cipher, mid-way through a collapsed 16-round one.
+#ifdef T3_KEYED_SYNC_EVERY  // (experiments)
+constexpr int T3K_SYNC_EVERY = T3_KEYED_SYNC_EVERY;
 #else
-#define T3_KEYED_SYNC() ((void)0)
+constexpr int T3K_SYNC_EVERY = 16;  // scripts/r2_keyed_ab{3,4}.sh
+#endif
+constexpr int T3K_SYNC = T3_KROUNDS <= T3K_SYNC_EVERY ? T3_KROUNDS / 2 : T3K_SYNC_EVERY;
+
+#ifdef __CUDA_ARCH__
+// A plain __syncthreads constrains no register dataflow, and ptxas hoists
+// every one of them to the top of the cipher (measured: all BAR.SYNC within
+// the first 0.5 KB of the ~180 KB body).  This barrier is pinned between its
+// rounds by a data dependency instead: its predicate reads the state and its
+// result feeds the state back through `z`, a kernel-parameter zero the
+// compiler cannot fold (one SEL + one LOP3 per barrier).
+#define T3_KEYED_SYNC_AB(A, B, z)                               \
+    {                                                           \
+        const int r_ = __syncthreads_or((B)[0] == 0x9E3779B9u); \
+        (A)[0] ^= r_ ? (z) : 0u;                                \
+    }
+#else
+#define T3_KEYED_SYNC_AB(A, B, z) ((void)(z))
 #endif
 
 template <int T>
-T3_FI void t3_keyed_rounds(uint32_t (&A)[32], uint32_t (&B)[32]) {
+T3_FI void t3_keyed_rounds(uint32_t (&A)[32], uint32_t (&B)[32], uint32_t z) {
     if constexpr (T < T3_KROUNDS) {
         if constexpr (T3K_ROLE[T] == 0)
             t3_keyed_round<T3_KSEQ[T]>(A, B);
         else
             t3_keyed_round<T3_KSEQ[T]>(B, A);
-        if constexpr ((T + 1) % T3_KEYED_SYNC_EVERY == 0 && T + 1 < T3_KROUNDS) T3_KEYED_SYNC();
-        t3_keyed_rounds<T + 1>(A, B);
+        if constexpr ((T + 1) % T3K_SYNC == 0 && T + 1 < T3_KROUNDS) T3_KEYED_SYNC_AB(A, B, z);
+        t3_keyed_rounds<T + 1>(A, B, z);
     }
 }
 
 // 32 blocks per thread: lo/hi = the big-endian halves as loaded (t3_tile32)
-T3_FI void t3_keyed_tile(uint32_t (&lo)[32], uint32_t (&hi)[32]) {
+T3_FI void t3_keyed_tile(uint32_t (&lo)[32], uint32_t (&hi)[32], uint32_t z = 0) {
     t3_transpose32<0>(lo);
     t3_transpose32<0>(hi);
     uint32_t A[32] = T3_GATHER_A(lo, hi);
     uint32_t B[32] = T3_GATHER_B(lo, hi);
-    t3_keyed_rounds<0>(A, B);
+    t3_keyed_rounds<0>(A, B, z);
     uint32_t olo[32] = T3_SCATTER_LO(A, B);
     uint32_t ohi[32] = T3_SCATTER_HI(A, B);
 #pragma unroll
@@ -74,7 +90,7 @@ T3_FI void t3_keyed_tile(uint32_t (&lo)[32], uint32_t (&hi)[32]) {
 // shared memory T3_KEYED_WARPS * 8 KiB (each warp's next tile streams in by
 // TMA while it computes, as in t3_bs_tma_kernel).
 extern "C" __global__ void __launch_bounds__(T3_KEYED_WARPS * 32, 1)
-t3_keyed_kernel(const uint8_t* in, uint8_t* out, uint64_t ntiles) {
+t3_keyed_kernel(const uint8_t* in, uint8_t* out, uint64_t ntiles, uint32_t zero) {
     extern __shared__ __align__(128) uint4 kslot[];  // [T3_KEYED_WARPS][512]
     __shared__ __align__(8) uint64_t bar[T3_KEYED_WARPS];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -115,7 +131,7 @@ t3_keyed_kernel(const uint8_t* in, uint8_t* out, uint64_t ntiles) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             t3_tma_fetch(sdst, in + next * (T3_TILE_BLOCKS * 8), T3_TILE_BLOCKS * 8, sbar);
         }
-        t3_keyed_tile(lo, hi);
+        t3_keyed_tile(lo, hi, zero);
         if (live) {
             uint4* dst = reinterpret_cast<uint4*>(out + tile * (T3_TILE_BLOCKS * 8)) + lane;
 #pragma unroll

@@ -17,7 +17,7 @@ import paper_1305_4376_b200 as t3  # noqa: E402
 
 n = (1 << 30) // 8
 e = t3.Engine(0)
-e.set_schedule(t3.triple_schedule(t3.parse_hex_key("133457799BBCDFF10E329232EA6D0D737CA110454A1A6E57")))
+e.set_schedule(t3.triple_schedule(t3.parse_hex_key(os.environ.get("T3_AB_KEY", "133457799BBCDFF10E329232EA6D0D737CA110454A1A6E57"))))
 x = torch.empty(8 * n, dtype=torch.uint8, device="cuda")
 e.fill_splitmix(x.data_ptr(), 0, n, 0x3DE5C0DE)
 s = torch.cuda.Stream()

@@ -108,7 +108,7 @@ def test_keyed_compile_sm100a_cubin(engine_lib, tmp_path):
     ops = [ln.split()[1].split(".")[0] for ln in sass.splitlines() if ln.strip().startswith("/*") and "*/" in ln
            and len(ln.split()) > 1]
     assert ops.count("LOP3") >= 48 * 186
-    assert ops.count("BAR") >= 3  # a barrier every 12 of the 48 rounds
+    assert ops.count("BAR") >= 2  # the CTA barriers pinned at the pass boundaries
     assert "UBLKCP" in ops
 
 
