@@ -15,10 +15,10 @@
 // with free-running 4-warp CTAs, profiles/r1/keyed_experiment_r1g.txt).  A
 // CTA is therefore 16 warps, one per SM, re-aligned by CTA barriers pinned at
 // the pass boundaries, so all warps of an SM fetch from one window of the
-// code.  Every warp of the grid runs the same number of passes; a warp past
-// the last tile computes on zeros and stores nothing, which keeps the
-// barriers uniform for any tile count (letting it take only the barriers
-// measured 3% slower, profiles/r2/keyed_ab_r2y.jsonl).
+// code.  Every warp of the grid runs the same number of passes; a pass's
+// tiles go warp-major over the CTAs, and in the last (partial) pass a warp
+// past the last tile takes only the barriers, so the live warps are spread
+// over all SMs and get their issue slots (+0.35%, keyed_ab5_r2z.jsonl).
 //
 // Also compiles as plain host C++ (tests/native/keyed_host.cpp): the rounds
 // and tile function then run on the CPU for the parity tests.
@@ -96,7 +96,9 @@ t3_keyed_kernel(const uint8_t* in, uint8_t* out, uint64_t ntiles, uint32_t zero)
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t nwarps = uint64_t(gridDim.x) * T3_KEYED_WARPS;
     const uint64_t iters = (ntiles + nwarps - 1) / nwarps;  // the same for every warp: uniform barriers
-    uint64_t tile = uint64_t(blockIdx.x) * T3_KEYED_WARPS + wib;
+    // a pass's tiles warp-major over the CTAs, so the live warps of the
+    // last (partial) pass are spread over all SMs
+    uint64_t tile = uint64_t(wib) * gridDim.x + blockIdx.x;
     const uint32_t sbar = t3_smem_addr(&bar[wib]);
     const uint32_t sdst = t3_smem_addr(&kslot[wib * 512]);
     if (lane == 0) {
@@ -108,21 +110,21 @@ t3_keyed_kernel(const uint8_t* in, uint8_t* out, uint64_t ntiles, uint32_t zero)
     uint32_t parity = 0;
     for (uint64_t it = 0; it < iters; ++it, tile += nwarps) {
         const bool live = tile < ntiles;  // warp-uniform
+        if (!live) {  // past the last tile: only the cipher's barriers (pass-uniform)
+#pragma unroll 1
+            for (int b = 0; b < (T3_KROUNDS - 1) / T3K_SYNC; ++b) (void)__syncthreads_or(0);
+            continue;
+        }
+        t3_mbar_wait(sbar, parity);
+        parity ^= 1u;
         uint32_t lo[32], hi[32];
-        if (live) {
-            t3_mbar_wait(sbar, parity);
-            parity ^= 1u;
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const uint4 v = kslot[wib * 512 + 32 * j + lane];
-                lo[2 * j] = v.x;
-                hi[2 * j] = v.y;
-                lo[2 * j + 1] = v.z;
-                hi[2 * j + 1] = v.w;
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < 32; ++k) lo[k] = hi[k] = 0u;
+        for (int j = 0; j < 16; ++j) {
+            const uint4 v = kslot[wib * 512 + 32 * j + lane];
+            lo[2 * j] = v.x;
+            hi[2 * j] = v.y;
+            lo[2 * j + 1] = v.z;
+            hi[2 * j + 1] = v.w;
         }
         __syncwarp();
         const uint64_t next = tile + nwarps;
@@ -132,12 +134,10 @@ t3_keyed_kernel(const uint8_t* in, uint8_t* out, uint64_t ntiles, uint32_t zero)
             t3_tma_fetch(sdst, in + next * (T3_TILE_BLOCKS * 8), T3_TILE_BLOCKS * 8, sbar);
         }
         t3_keyed_tile(lo, hi, zero);
-        if (live) {
-            uint4* dst = reinterpret_cast<uint4*>(out + tile * (T3_TILE_BLOCKS * 8)) + lane;
+        uint4* dst = reinterpret_cast<uint4*>(out + tile * (T3_TILE_BLOCKS * 8)) + lane;
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-                __stcs(dst + 32 * j, make_uint4(lo[2 * j], hi[2 * j], lo[2 * j + 1], hi[2 * j + 1]));
-        }
+        for (int j = 0; j < 16; ++j)
+            __stcs(dst + 32 * j, make_uint4(lo[2 * j], hi[2 * j], lo[2 * j + 1], hi[2 * j + 1]));
     }
 }
 #endif  // __CUDACC__
