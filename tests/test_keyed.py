@@ -230,3 +230,30 @@ def test_keyed_variant_in_a_cuda_graph(keng, oracle):
     torch.cuda.synchronize()
     assert np.array_equal(y.cpu().numpy(), oracle.ecb(x, oracle.schedule_hex(key), 0))
     assert torch.equal(z, xd)
+
+
+@pytest.mark.gpu
+def test_keyed_variant_fuzz(keng, oracle):
+    """Random keys of all three keying shapes, random sizes (whole tiles,
+    passes with idle warps, tails), random 16-byte-aligned offsets, both
+    directions, in place or not — the keyed variant against the oracle."""
+    rng = random.Random(0xF4)
+    for trial in range(6):
+        nhex = rng.choice([16, 32, 48])
+        key = "".join(rng.choice("0123456789ABCDEF") for _ in range(nhex))
+        s = oracle.schedule_hex(key)
+        for _ in range(3):
+            n = rng.choice([1024 * rng.randint(1, 3000), rng.randint(1, 4_000_000)])
+            direction = rng.randint(0, 1)
+            off = 16 * rng.randint(0, 8)  # blocks stay 16-byte aligned: the keyed kernel runs
+            x = oracle.splitmix(0, n, rng.getrandbits(32))
+            buf = torch.zeros(off + x.nbytes + 64, dtype=torch.uint8, device="cuda")
+            src = buf[off: off + x.nbytes]
+            src.copy_(torch.from_numpy(x))
+            if rng.random() < 0.5:
+                _run(keng, key, src, direction, out=src)
+                got = src.cpu().numpy()
+            else:
+                got = _run(keng, key, src, direction).cpu().numpy()
+            assert np.array_equal(got, oracle.ecb(x, s, direction)), (trial, key, n, direction, off)
+            assert not buf[off + x.nbytes:].any()  # nothing written past the batch
