@@ -97,15 +97,24 @@ class ClockSampler:
                 idx = int(vis.split(",")[self.device]) if vis else self.device
                 h = pynvml.nvmlDeviceGetHandleByIndex(idx)
             self._nvml = (pynvml, h)
+            self._ready = threading.Event()
             self._t = threading.Thread(target=self._loop, daemon=True)
             self._t.start()
+            # the sampler's first NVML queries can take longer than a short
+            # timed region (one fresh box gave 0 samples over 54 ms): start
+            # timing only once it is sampling
+            self._ready.wait(timeout=5.0)
+            self.samples.clear()
         except Exception:
             self._nvml = None
         return self
 
     def _loop(self):
         pynvml, h = self._nvml
-        mx = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+        try:
+            mx = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+        except Exception:
+            mx = float("nan")
         while not self._stop.is_set():
             try:
                 sm = float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
@@ -113,12 +122,21 @@ class ClockSampler:
                 self.samples.append((sm, mx, rs))
             except Exception:
                 pass
+            self._ready.set()
             time.sleep(0.002)
 
     def __exit__(self, *exc):
         self._stop.set()
         if self._t:
             self._t.join(timeout=2)
+        if self._nvml and not self.samples:  # still none: one read as the region ends
+            pynvml, h = self._nvml
+            try:
+                self.samples.append((float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)),
+                                     float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)),
+                                     int(pynvml.nvmlDeviceGetCurrentClocksEventReasons(h))))
+            except Exception:
+                pass
 
     def summary(self) -> dict:
         if not self.samples:
