@@ -13,6 +13,15 @@
 //   dispatch.hpp:44-47, tdes.hpp:25-28  InputLengthError, KeyFormatError
 //   dispatch.hpp:32,49-91  PaddingMode, PaddingError, IoError, StreamReport,
 //                      encrypt_stream/decrypt_stream, pkcs7_pad/pkcs7_unpad
+//   dispatch.hpp:94    resolve_workers                  same (GPU shards)
+//   tdes.hpp:34        to_hex                           same format
+//   des.hpp:25-28,41-48  ParityError, has_odd_parity, normalize_parity,
+//                      is_weak_key, is_semiweak_key     same semantics
+//   des.hpp:37-39, tdes.hpp:44-54  encrypt_block/decrypt_block,
+//                      tdes_{en,de}crypt_block[_fast]   one block through the
+//                                                       device (see below)
+//   verify.hpp:14-37   DesKat, TdesKat, des_kats, tdes_kats,
+//                      walkthrough_subkeys, kWalkthroughKey, run_verification
 //
 // Backend::Cuda sends the whole batch through the C ABI (t3des_cu.h) in
 // one call; there is no CPU cipher in this library (ScalarReference and
@@ -73,8 +82,21 @@ class CudaError : public std::runtime_error {
     int status;
 };
 
+class ParityError : public std::runtime_error {
+  public:
+    using std::runtime_error::runtime_error;
+};
+
 TripleKey parse_hex_key(std::string_view hex);
+std::string to_hex(const TripleKey& key);
 RoundKeySet key_schedule(DesKey key);
+
+// Key hygiene (host only): odd parity in the LSB of every byte; the 4 weak
+// and 12 semi-weak keys compared with the parity bits masked off.
+bool has_odd_parity(DesKey key);
+DesKey normalize_parity(DesKey key);
+bool is_weak_key(DesKey key);
+bool is_semiweak_key(DesKey key);
 
 struct TripleSchedule {
     RoundKeySet pass1, pass2, pass3;
@@ -110,6 +132,10 @@ struct ChunkSpan {
 };
 
 std::vector<ChunkSpan> plan_dispatch(std::size_t total_blocks, const DispatchConfig& cfg);
+
+// Backend::Cuda: the number of block-range shards a batch is split into
+// (workers == 0 means 1; each shard runs on its own GPU context).
+unsigned resolve_workers(const DispatchConfig& cfg);
 
 void encrypt_batch(std::span<const std::uint8_t> in, std::span<std::uint8_t> out,
                    const TripleSchedule& ts, const DispatchConfig& cfg);
@@ -152,5 +178,43 @@ StreamReport decrypt_stream(std::istream& source, std::ostream& sink, const Trip
 // PKCS#7 over 8-byte blocks: always appends 1..8 bytes; unpad throws PaddingError.
 void pkcs7_pad(std::vector<std::uint8_t>& data);
 void pkcs7_unpad(std::vector<std::uint8_t>& data);
+
+// Single-block transforms with the reference's signatures.  This library
+// has no CPU cipher: each call is a one-block batch through the engine on
+// device 0 (tens of microseconds), for code ported from the reference that
+// checks a block or two; bulk work belongs in encrypt_batch/decrypt_batch.
+// encrypt_block/decrypt_block are single DES under one 16-key schedule
+// (run as the collapsed EDE (ks, ks, ks)); the _fast names equal the plain
+// ones, as the reference's two routes do.
+Block encrypt_block(Block block, const RoundKeySet& ks);
+Block decrypt_block(Block block, const RoundKeySet& ks);
+Block tdes_encrypt_block(Block block, const TripleSchedule& ts);
+Block tdes_decrypt_block(Block block, const TripleSchedule& ts);
+Block tdes_encrypt_block_fast(Block block, const TripleSchedule& ts);
+Block tdes_decrypt_block_fast(Block block, const TripleSchedule& ts);
+
+// Known-answer vectors and the self-check behind the CLI's `verify`.
+struct DesKat {
+    std::uint64_t key;
+    std::uint64_t plaintext;
+    std::uint64_t ciphertext;
+};
+
+struct TdesKat {
+    std::string_view key_hex;
+    std::string_view plaintext_hex;  // one block
+    std::string_view ciphertext_hex;
+};
+
+std::span<const DesKat> des_kats();
+std::span<const TdesKat> tdes_kats();
+std::span<const std::uint64_t> walkthrough_subkeys();
+constexpr std::uint64_t kWalkthroughKey = 0x133457799BBCDFF1ull;
+
+// Runs the vectors and structural properties (round trips, EDE collapse,
+// complementation) on the GPU named by cfg (Backend::Cuda); one line per
+// group, then "verification PASSED" / "verification FAILED".
+bool run_verification(std::ostream& out);
+bool run_verification(std::ostream& out, const DispatchConfig& cfg);
 
 }  // namespace t3des

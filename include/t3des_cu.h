@@ -91,6 +91,19 @@ int t3des_cu_parse_hex_key(const char* hex, size_t len, uint64_t keys[3], int* o
  * reference's TripleSchedule {pass1, pass2, pass3} (tdes.hpp:38-40). */
 int t3des_cu_triple_schedule(const uint64_t keys[3], uint64_t sub48[48]);
 
+/* Key hygiene, replacing has_odd_parity / is_weak_key / is_semiweak_key
+ * (des.hpp:41-48; des.cpp:159-207): a bit mask of the T3DES_CU_KEY_* flags
+ * below for one 64-bit DES key.  Weak and semi-weak keys are compared with
+ * the parity bits (the LSB of every byte) masked off, as in the reference. */
+#define T3DES_CU_KEY_ODD_PARITY 1 /* every byte has odd parity        */
+#define T3DES_CU_KEY_WEAK 2       /* one of the 4 weak keys           */
+#define T3DES_CU_KEY_SEMIWEAK 4   /* one of the 12 semi-weak keys     */
+int t3des_cu_des_key_flags(uint64_t key);
+
+/* Replaces normalize_parity (des.hpp:42; des.cpp:167-175): flips the LSB of
+ * every byte whose parity is even. */
+uint64_t t3des_cu_normalize_parity(uint64_t key);
+
 /* ---- contexts ------------------------------------------------------------ */
 
 int t3des_cu_device_count(int* count);

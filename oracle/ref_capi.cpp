@@ -96,6 +96,25 @@ unsigned ref_resolve_workers(unsigned workers) {
     return resolve_workers(cfg);
 }
 
+// Key hygiene (des.hpp:41-48): bit 0 odd parity, bit 1 weak, bit 2 semi-weak.
+int ref_key_flags(std::uint64_t k) {
+    const DesKey key{k};
+    return (has_odd_parity(key) ? 1 : 0) | (is_weak_key(key) ? 2 : 0) | (is_semiweak_key(key) ? 4 : 0);
+}
+
+std::uint64_t ref_normalize_parity(std::uint64_t k) { return normalize_parity(DesKey{k}).raw; }
+
+// to_hex(parse_hex_key(hex)) (tdes.hpp:32-34) into out (>= 49 bytes).
+int ref_to_hex(const char* hex, char* out) {
+    try {
+        const std::string s = to_hex(parse_hex_key(std::string_view(hex)));
+        std::memcpy(out, s.c_str(), s.size() + 1);
+        return 0;
+    } catch (const std::exception& e) {
+        return to_code(e);
+    }
+}
+
 int ref_run_verification(void) {
     std::ostringstream os;
     return run_verification(os) ? 0 : 1;

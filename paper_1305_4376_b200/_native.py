@@ -39,6 +39,9 @@ VARIANT_KEYED = 7  # key-specialised, NVRTC-compiled at run time (opt-in)
 AUTO_SMALL_BLOCKS = 131072
 MULTI_STAGE_ALL = 1  # t3des_cu_ecb_multi_device flags
 MULTI_COPY = 2
+KEY_ODD_PARITY = 1  # t3des_cu_des_key_flags bits
+KEY_WEAK = 2
+KEY_SEMIWEAK = 4
 
 class StreamReportC(ctypes.Structure):
     """t3des_cu_stream_report (include/t3des_cu.h)."""
@@ -58,6 +61,8 @@ SIGNATURES = {
     "t3des_cu_strerror": (ctypes.c_char_p, [_i]),
     "t3des_cu_parse_hex_key": (_i, [ctypes.c_char_p, _sz, _u64p, ctypes.POINTER(_i)]),
     "t3des_cu_triple_schedule": (_i, [_u64p, _u64p]),
+    "t3des_cu_des_key_flags": (_i, [ctypes.c_uint64]),
+    "t3des_cu_normalize_parity": (ctypes.c_uint64, [ctypes.c_uint64]),
     "t3des_cu_device_count": (_i, [ctypes.POINTER(_i)]),
     "t3des_cu_create": (_i, [_i, ctypes.POINTER(_vp)]),
     "t3des_cu_destroy": (_i, [_vp]),

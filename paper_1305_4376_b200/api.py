@@ -141,6 +141,34 @@ def triple_schedule(key: TripleKey) -> TripleSchedule:
     return TripleSchedule(tuple(s[:16]), tuple(s[16:32]), tuple(s[32:]))
 
 
+class ParityError(ValueError):
+    """des.hpp:25-28 (raised by callers that enforce odd parity, e.g. the CLI's --check-parity)."""
+
+
+def _raw(key) -> int:
+    return key.raw if isinstance(key, DesKey) else int(key)
+
+
+def has_odd_parity(key) -> bool:
+    """des.hpp:42: every byte of the 64-bit key has odd parity."""
+    return bool(N.lib().t3des_cu_des_key_flags(_raw(key)) & N.KEY_ODD_PARITY)
+
+
+def normalize_parity(key) -> DesKey:
+    """des.hpp:43: the LSB of each even-parity byte flipped."""
+    return DesKey(int(N.lib().t3des_cu_normalize_parity(_raw(key))))
+
+
+def is_weak_key(key) -> bool:
+    """des.hpp:47: one of the 4 weak keys (parity bits masked)."""
+    return bool(N.lib().t3des_cu_des_key_flags(_raw(key)) & N.KEY_WEAK)
+
+
+def is_semiweak_key(key) -> bool:
+    """des.hpp:48: one of the 12 semi-weak keys (parity bits masked)."""
+    return bool(N.lib().t3des_cu_des_key_flags(_raw(key)) & N.KEY_SEMIWEAK)
+
+
 def load_block(b: bytes) -> int:
     return int.from_bytes(bytes(b[:8]), "big")
 
@@ -176,6 +204,11 @@ class ChunkSpan:
 def plan_dispatch(total_blocks: int, cfg: DispatchConfig) -> list[ChunkSpan]:
     step = cfg.chunk_blocks or max(total_blocks, 1)
     return [ChunkSpan(o, min(step, total_blocks - o)) for o in range(0, total_blocks, step)]
+
+
+def resolve_workers(cfg: DispatchConfig) -> int:
+    """dispatch.hpp:94 on Backend::CUDA: block-range shards per batch (0 -> 1)."""
+    return cfg.workers or 1
 
 
 class Engine:
@@ -401,6 +434,42 @@ def decrypt_batch(src, dst, ts: TripleSchedule, cfg: DispatchConfig | None = Non
 
 
 # ---- streams (dispatch.hpp:32,71-91) ----------------------
+
+def _one_block(block: int, ts: TripleSchedule, direction: int) -> int:
+    buf = bytearray(store_block(block))
+    _run_batch(buf, buf, ts, DispatchConfig(), direction)
+    return load_block(buf)
+
+
+def _single(ks) -> TripleSchedule:
+    ks = tuple(ks)
+    return TripleSchedule(ks, ks, ks)
+
+
+def encrypt_block(block: int, ks) -> int:
+    """des.hpp:37: single DES of one block under a 16-key schedule, as a
+    one-block batch through the engine (EDE of (ks, ks, ks))."""
+    return _one_block(block, _single(ks), N.ENCRYPT)
+
+
+def decrypt_block(block: int, ks) -> int:
+    """des.hpp:38 (see encrypt_block)."""
+    return _one_block(block, _single(ks), N.DECRYPT)
+
+
+def tdes_encrypt_block(block: int, ts: TripleSchedule) -> int:
+    """tdes.hpp:46: one block through the engine (bulk work: encrypt_batch)."""
+    return _one_block(block, ts, N.ENCRYPT)
+
+
+def tdes_decrypt_block(block: int, ts: TripleSchedule) -> int:
+    """tdes.hpp:47: one block through the engine (bulk work: decrypt_batch)."""
+    return _one_block(block, ts, N.DECRYPT)
+
+
+tdes_encrypt_block_fast = tdes_encrypt_block  # tdes.hpp:53: the same function
+tdes_decrypt_block_fast = tdes_decrypt_block  # tdes.hpp:54
+
 
 class PaddingMode(enum.Enum):
     NONE = 0

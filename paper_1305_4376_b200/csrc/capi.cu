@@ -513,6 +513,13 @@ int t3des_cu_triple_schedule(const std::uint64_t keys[3], std::uint64_t sub48[48
     return T3DES_CU_OK;
 }
 
+int t3des_cu_des_key_flags(std::uint64_t key) {
+    return (t3b::has_odd_parity(key) ? T3DES_CU_KEY_ODD_PARITY : 0) | (t3b::is_weak_key(key) ? T3DES_CU_KEY_WEAK : 0) |
+           (t3b::is_semiweak_key(key) ? T3DES_CU_KEY_SEMIWEAK : 0);
+}
+
+std::uint64_t t3des_cu_normalize_parity(std::uint64_t key) { return t3b::normalize_parity(key); }
+
 int t3des_cu_device_count(int* count) {
     if (!count) return T3DES_CU_ERR_ARG;
     int n = 0;

@@ -25,31 +25,10 @@ namespace {
 constexpr int kExitIo = 1, kExitUsage = 2, kExitKeyFormat = 3, kExitInputLength = 4, kExitPadding = 5,
               kExitParity = 6, kExitVerifyFailed = 7;
 
-struct ParityError : std::runtime_error {
-    using std::runtime_error::runtime_error;
-};
+using t3des::ParityError;
 struct UsageError : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
-
-// ---- key hygiene (reference des.cpp:159-207, CLI-only) -------------------
-bool odd_parity(std::uint64_t k) {
-    for (int i = 0; i < 8; ++i)
-        if (__builtin_popcount(static_cast<unsigned>((k >> (8 * i)) & 0xFF)) % 2 == 0) return false;
-    return true;
-}
-
-bool weak_or_semiweak(std::uint64_t k) {
-    static const std::uint64_t kList[] = {
-        0x0101010101010101ull, 0xFEFEFEFEFEFEFEFEull, 0xE0E0E0E0F1F1F1F1ull, 0x1F1F1F1F0E0E0E0Eull,
-        0x01FE01FE01FE01FEull, 0xFE01FE01FE01FE01ull, 0x1FE01FE00EF10EF1ull, 0xE01FE01FF10EF10Eull,
-        0x01E001E001F101F1ull, 0xE001E001F101F101ull, 0x1FFE1FFE0EFE0EFEull, 0xFE1FFE1FFE0EFE0Eull,
-        0x011F011F010E010Eull, 0x1F011F010E010E01ull, 0xE0FEE0FEF1FEF1FEull, 0xFEE0FEE0FEF1FEF1ull};
-    const std::uint64_t m = 0xFEFEFEFEFEFEFEFEull;  // parity bits masked
-    for (std::uint64_t w : kList)
-        if ((k & m) == (w & m)) return true;
-    return false;
-}
 
 struct Opts {
     std::string cmd;
@@ -152,9 +131,9 @@ t3des::TripleKey load_key(const Opts& o) {
     if (hex.empty()) throw t3des::KeyFormatError("a key is required (--key or --key-file)");
     t3des::TripleKey key = t3des::parse_hex_key(hex);
     for (const t3des::DesKey& k : {key.k1, key.k2, key.k3}) {
-        if (o.check_parity && !odd_parity(k.raw))
+        if (o.check_parity && !t3des::has_odd_parity(k))
             throw ParityError("key byte fails odd-parity check (--check-parity)");
-        if (weak_or_semiweak(k.raw)) {
+        if (t3des::is_weak_key(k) || t3des::is_semiweak_key(k)) {
             if (o.strict_keys) throw t3des::KeyFormatError("weak or semi-weak DES key rejected (--strict-keys)");
             std::cerr << "warning: key component is a weak or semi-weak DES key\n";
         }
@@ -209,89 +188,9 @@ int run_crypt(const Opts& o, bool encrypt) {
 }
 
 // ---- verify: known answers and structural properties, on the GPU --------
-std::vector<std::uint8_t> be(std::uint64_t v) {
-    std::vector<std::uint8_t> b(8);
-    for (int i = 0; i < 8; ++i) b[i] = static_cast<std::uint8_t>(v >> (56 - 8 * i));
-    return b;
-}
-
+// (the library's t3des::run_verification, verify_api.cpp)
 int run_verify(const Opts& o) {
-    const t3des::DispatchConfig cfg = make_config(o);
-    bool all = true;
-    auto check = [&](const char* name, bool pass) {
-        std::cout << (pass ? "ok   " : "FAIL ") << name << '\n';
-        all &= pass;
-    };
-    // the classic walkthrough schedule (reference verify.cpp:35-40)
-    const std::uint64_t walk[16] = {0x1B02EFFC7072, 0x79AED9DBC9E5, 0x55FC8A42CF99, 0x72ADD6DB351D,
-                                    0x7CEC07EB53A8, 0x63A53E507B2F, 0xEC84B7F618BC, 0xF78A3AC13BFB,
-                                    0xE0DBEBEDE781, 0xB1F347BA464F, 0x215FD3DED386, 0x7571F59467E9,
-                                    0x97C5D1FABA41, 0x5F43B7F2E73A, 0xBF918D3D3F0A, 0xCB3D8B0E17F5};
-    const auto ks = t3des::key_schedule(t3des::DesKey{0x133457799BBCDFF1ull});
-    check("walkthrough subkeys", std::equal(ks.begin(), ks.end(), walk));
-    struct Kat {
-        const char* key;
-        const char* pt;
-        const char* ct;
-    };
-    // DES vectors as option-3 keys (EDE collapses to DES), TDES vectors for
-    // all keying options and the 3-block NIST SP 800-67 example.
-    const Kat kats[] = {
-        {"133457799BBCDFF1", "0123456789ABCDEF", "85E813540F0AB405"},
-        {"0E329232EA6D0D73", "8787878787878787", "0000000000000000"},
-        {"0101010101010101", "0000000000000000", "8CA64DE9C1B123A7"},
-        {"8001010101010101", "0000000000000000", "95A8D72813DAA94D"},
-        {"7CA110454A1A6E57", "01A1D6D039776742", "690F5B0D9A26939B"},
-        {"0131D9619DC1376E", "5CD54CA83DEF57DA", "7A389D10354BD271"},
-        {"0123456789ABCDEF23456789ABCDEF01456789ABCDEF0123", "5468652071756663", "A826FD8CE53B855F"},
-        {"133457799BBCDFF10E329232EA6D0D737CA110454A1A6E57", "0123456789ABCDEF", "1A493D768C1B9432"},
-        {"0123456789ABCDEF23456789ABCDEF01", "4E6F772069732074", "B7835779EE26ACB7"},
-        {"0123456789ABCDEF", "4E6F772069732074", "3FA40E8A984D4815"},
-        {"0123456789ABCDEF23456789ABCDEF01456789ABCDEF0123",
-         "54686520717566636B2062726F776E20666F78206A756D70",
-         "A826FD8CE53B855FCCE21C8112256FE668D5C05DD9B6B900"},
-    };
-    auto unhex = [](const std::string& h) {
-        std::vector<std::uint8_t> b(h.size() / 2);
-        for (std::size_t i = 0; i < b.size(); ++i) b[i] = static_cast<std::uint8_t>(std::stoul(h.substr(2 * i, 2), nullptr, 16));
-        return b;
-    };
-    bool kat_ok = true;
-    for (const Kat& k : kats) {
-        const auto ts = t3des::triple_schedule(t3des::parse_hex_key(k.key));
-        auto pt = unhex(k.pt), want = unhex(k.ct);
-        std::vector<std::uint8_t> ct(pt.size()), back(pt.size());
-        t3des::encrypt_batch(pt, ct, ts, cfg);
-        t3des::decrypt_batch(ct, back, ts, cfg);
-        kat_ok &= ct == want && back == pt;
-    }
-    check("known-answer vectors (DES via option 3, TDES options 1/2/3, SP 800-67)", kat_ok);
-    // round trips and the complementation property E_{~k}(~x) = ~E_k(x),
-    // 256 random 3-key cases in one batch each
-    std::mt19937_64 rng(0x5EED);
-    bool rt = true, comp = true;
-    for (int i = 0; i < 256; ++i) {
-        t3des::TripleKey key;
-        key.k1.raw = rng();
-        key.k2.raw = rng();
-        key.k3.raw = rng();
-        t3des::TripleKey nkey = key;
-        nkey.k1.raw = ~key.k1.raw;
-        nkey.k2.raw = ~key.k2.raw;
-        nkey.k3.raw = ~key.k3.raw;
-        std::vector<std::uint8_t> x(8 * 33), y(x.size()), z(x.size()), nx(x.size()), ny(x.size());
-        for (auto& b : x) b = static_cast<std::uint8_t>(rng());
-        for (std::size_t j = 0; j < x.size(); ++j) nx[j] = static_cast<std::uint8_t>(~x[j]);
-        const auto ts = t3des::triple_schedule(key);
-        t3des::encrypt_batch(x, y, ts, cfg);
-        t3des::decrypt_batch(y, z, ts, cfg);
-        rt &= z == x;
-        t3des::encrypt_batch(nx, ny, t3des::triple_schedule(nkey), cfg);
-        for (std::size_t j = 0; j < x.size(); ++j) comp &= ny[j] == static_cast<std::uint8_t>(~y[j]);
-    }
-    check("256 random 3-key round trips", rt);
-    check("complementation property", comp);
-    return all ? 0 : kExitVerifyFailed;
+    return t3des::run_verification(std::cout, make_config(o)) ? 0 : kExitVerifyFailed;
 }
 
 // ---- bench: GPU sweeps shaped like the reference's Tables I/II/IV ---------

@@ -210,4 +210,46 @@ void build_sp_tables(std::uint32_t sp[8][64]) {
         }
 }
 
+// ---- key hygiene ----------------------------------------------------------
+// Parity: FIPS 46-3 DES keys carry odd parity in the LSB of each byte.
+bool has_odd_parity(std::uint64_t key) {
+    for (int i = 0; i < 8; ++i)
+        if (!__builtin_parity(static_cast<unsigned>((key >> (8 * i)) & 0xFFu))) return false;
+    return true;
+}
+
+std::uint64_t normalize_parity(std::uint64_t key) {
+    for (int i = 0; i < 8; ++i)
+        if (!__builtin_parity(static_cast<unsigned>((key >> (8 * i)) & 0xFFu))) key ^= std::uint64_t(1) << (8 * i);
+    return key;
+}
+
+// Weak and semi-weak keys, characterised by what makes them weak instead of
+// listed: after PC-1 (which drops the parity bits) each 28-bit register C, D
+// is invariant under the schedule's rotations (all zeros or all ones: the 16
+// subkeys are identical, the 4 weak keys) or 2-periodic (0101... / 1010...:
+// the subkeys alternate between two values).  The 4 x 4 combinations minus
+// the 4 weak ones are the 12 semi-weak keys of the reference's table
+// (des.cpp:180-191); tests/test_capi_host.py checks the two agree.
+namespace {
+int register_class(std::uint32_t r) {  // 0: constant, 1: 2-periodic, -1: other
+    if (r == 0 || r == 0x0FFFFFFFu) return 0;
+    if (r == 0x05555555u || r == 0x0AAAAAAAu) return 1;
+    return -1;
+}
+}  // namespace
+
+bool is_weak_key(std::uint64_t key) {
+    const std::uint64_t cd = gather_bits(key, 64, kPC1, 56);
+    return register_class(static_cast<std::uint32_t>(cd >> 28)) == 0 &&
+           register_class(static_cast<std::uint32_t>(cd) & 0x0FFFFFFFu) == 0;
+}
+
+bool is_semiweak_key(std::uint64_t key) {
+    const std::uint64_t cd = gather_bits(key, 64, kPC1, 56);
+    const int c = register_class(static_cast<std::uint32_t>(cd >> 28));
+    const int d = register_class(static_cast<std::uint32_t>(cd) & 0x0FFFFFFFu);
+    return c >= 0 && d >= 0 && (c | d) == 1;
+}
+
 }  // namespace t3b

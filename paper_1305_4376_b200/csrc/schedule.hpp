@@ -55,4 +55,12 @@ void build_sp_keys(const std::uint64_t seq[48], SpKeys& out);
 // The eight S-box/P fused tables (2 KiB): sp[i][six] = P(S_i(six) placed).
 void build_sp_tables(std::uint32_t sp[8][64]);
 
+// Key hygiene (reference des.cpp:159-207, semantics restated): every byte
+// of odd parity; the LSB of even-parity bytes flipped; membership in the 4
+// weak / 12 semi-weak keys with the parity bits masked off.
+bool has_odd_parity(std::uint64_t key);
+std::uint64_t normalize_parity(std::uint64_t key);
+bool is_weak_key(std::uint64_t key);
+bool is_semiweak_key(std::uint64_t key);
+
 }  // namespace t3b

@@ -182,6 +182,23 @@ TripleKey parse_hex_key(std::string_view hex) {
     return key;
 }
 
+// Reference to_hex (tdes.hpp:34): upper-case hex of the keys the option
+// carries (k1 k2 k3 / k1 k2 / k1).
+std::string to_hex(const TripleKey& key) {
+    const int n = key.option == KeyingOption::Option1 ? 3 : (key.option == KeyingOption::Option2 ? 2 : 1);
+    const std::uint64_t k[3] = {key.k1.raw, key.k2.raw, key.k3.raw};
+    static const char digits[] = "0123456789ABCDEF";
+    std::string s;
+    for (int i = 0; i < n; ++i)
+        for (int nib = 15; nib >= 0; --nib) s += digits[(k[i] >> (4 * nib)) & 0xF];
+    return s;
+}
+
+bool has_odd_parity(DesKey key) { return t3des_cu_des_key_flags(key.raw) & T3DES_CU_KEY_ODD_PARITY; }
+DesKey normalize_parity(DesKey key) { return DesKey{t3des_cu_normalize_parity(key.raw)}; }
+bool is_weak_key(DesKey key) { return t3des_cu_des_key_flags(key.raw) & T3DES_CU_KEY_WEAK; }
+bool is_semiweak_key(DesKey key) { return t3des_cu_des_key_flags(key.raw) & T3DES_CU_KEY_SEMIWEAK; }
+
 RoundKeySet key_schedule(DesKey key) {
     RoundKeySet ks{};
     t3b::des_key_schedule(key.raw, ks.data());
@@ -209,6 +226,8 @@ std::vector<ChunkSpan> plan_dispatch(std::size_t total_blocks, const DispatchCon
         spans.push_back(ChunkSpan{off, step < total_blocks - off ? step : total_blocks - off});
     return spans;
 }
+
+unsigned resolve_workers(const DispatchConfig& cfg) { return cfg.workers ? cfg.workers : 1u; }
 
 void encrypt_batch(std::span<const std::uint8_t> in, std::span<std::uint8_t> out, const TripleSchedule& ts,
                    const DispatchConfig& cfg) {

@@ -166,3 +166,91 @@ def test_pipeline_and_launch_argument_checks(engine_lib):
     sub = (ctypes.c_uint64 * 48)()
     assert L.t3des_cu_ecb_multi(devs, 1, sub, 0, None, None, 12) == N.ERR_LENGTH
     assert L.t3des_cu_ecb_multi_device(devs, 1, sub, 0, 0, None, None, 12, 0) == N.ERR_LENGTH
+
+
+def _key_hygiene_golden():
+    import json
+
+    with open(os.path.join(ROOT, "tests", "golden", "key_hygiene.json")) as f:
+        return json.load(f)
+
+
+def test_key_hygiene_matches_reference_golden(engine_lib):
+    """has_odd_parity / is_weak_key / is_semiweak_key / normalize_parity
+    (reference des.cpp:159-207) against the reference's own answers
+    (tests/golden/make_key_hygiene.py): the weak, semi-weak and 4-periodic
+    "possibly weak" register families with random parity bits, random keys."""
+    g = _key_hygiene_golden()
+    assert len(g["keys"]) > 1000
+    for hexkey, flags, normalized in g["keys"]:
+        k = int(hexkey, 16)
+        assert engine_lib.t3des_cu_des_key_flags(k) == flags, hexkey
+        assert engine_lib.t3des_cu_normalize_parity(k) == int(normalized, 16), hexkey
+        assert t3.has_odd_parity(k) == bool(flags & 1)
+        assert t3.is_weak_key(t3.DesKey(k)) == bool(flags & 2)
+        assert t3.is_semiweak_key(k) == bool(flags & 4)
+        assert t3.normalize_parity(k).raw == int(normalized, 16)
+        assert t3.has_odd_parity(t3.normalize_parity(k))
+    for case in g["to_hex"]:
+        assert t3.to_hex(t3.parse_hex_key(case["in"])) == case["to_hex"]
+
+
+def test_key_hygiene_matches_reference_library(engine_lib):
+    """The same against the reference library itself on fresh random keys
+    (skipped where oracle/_ref was not built)."""
+    from tests.oracle_util import REF_SO
+
+    if not os.path.exists(REF_SO):
+        pytest.skip("oracle/_ref not built (no /root/reference here)")
+    ref = ctypes.CDLL(REF_SO)
+    ref.ref_key_flags.argtypes = [ctypes.c_uint64]
+    ref.ref_key_flags.restype = ctypes.c_int
+    ref.ref_normalize_parity.argtypes = [ctypes.c_uint64]
+    ref.ref_normalize_parity.restype = ctypes.c_uint64
+    rng = np.random.default_rng(0xB200)
+    keys = [int(x) for x in rng.integers(0, 2**63, size=20000, dtype=np.uint64)]
+    keys += [k | (1 << 63) for k in keys[:100]]
+    for k in keys:
+        assert engine_lib.t3des_cu_des_key_flags(k) == ref.ref_key_flags(k), hex(k)
+        assert engine_lib.t3des_cu_normalize_parity(k) == ref.ref_normalize_parity(k), hex(k)
+
+
+def test_cpp_api_reference_surface(engine_lib, tmp_path):
+    """The rest of the reference's host API in the C++ mirror: to_hex,
+    ParityError, the key hygiene helpers, resolve_workers and the KAT
+    accessors compile, link and answer like the reference (no device)."""
+    g = _key_hygiene_golden()
+    src = tmp_path / "surface.cpp"
+    src.write_text(r'''
+#include <cstdio>
+#include <string>
+#include "t3des_b200/t3des.hpp"
+using namespace t3des;
+int main(int argc, char** argv) {
+    if (to_hex(parse_hex_key(argv[1])) != argv[2]) return 2;
+    const DesKey k{std::stoull(argv[3], nullptr, 16)};
+    const int flags = (has_odd_parity(k) ? 1 : 0) | (is_weak_key(k) ? 2 : 0) | (is_semiweak_key(k) ? 4 : 0);
+    if (flags != std::atoi(argv[4])) return 3;
+    if (normalize_parity(k).raw != std::stoull(argv[5], nullptr, 16)) return 4;
+    try { throw ParityError("x"); } catch (const std::runtime_error&) {}
+    DispatchConfig cfg;
+    if (resolve_workers(cfg) != 1) return 5;
+    cfg.workers = 3;
+    if (resolve_workers(cfg) != 3) return 6;
+    if (des_kats().size() != 6 || tdes_kats().size() != 4 || walkthrough_subkeys().size() != 16) return 7;
+    const auto ks = key_schedule(DesKey{kWalkthroughKey});
+    for (int i = 0; i < 16; ++i) if (ks[i] != walkthrough_subkeys()[i]) return 8;
+    std::puts("ok");
+    return 0;
+}
+''')
+    exe = tmp_path / "surface"
+    subprocess.check_call(["/usr/bin/g++", "-std=c++20", "-I" + os.path.join(ROOT, "include"), str(src),
+                           N.LIB_PATH, "-Wl,-rpath," + os.path.dirname(N.LIB_PATH), "-o", str(exe)])
+    weak = next(c for c in g["keys"] if c[1] & 2)
+    semi = next(c for c in g["keys"] if c[1] & 4)
+    plain = next(c for c in g["keys"] if c[1] == 0)
+    for case, key in zip(g["to_hex"][::4], (weak, semi, plain)):
+        p = subprocess.run([str(exe), case["in"], case["to_hex"], key[0], str(key[1]), key[2]],
+                           capture_output=True, text=True)
+        assert p.returncode == 0 and p.stdout.strip() == "ok", (p.returncode, case, key)
