@@ -104,6 +104,15 @@ int t3des_cu_des_key_flags(uint64_t key);
  * every byte whose parity is even. */
 uint64_t t3des_cu_normalize_parity(uint64_t key);
 
+/* Replaces run_verification (verify.hpp:37; verify.cpp:65-124) for C and
+ * ctypes callers: the walkthrough schedule, DES/3DES known answers, round
+ * trips, complementation and the EDE collapse, on `device`.  The report
+ * (one line per group, then "verification PASSED"/"FAILED") is copied into
+ * `report` (NUL-terminated, truncated to `capacity`) when non-null.  Returns
+ * T3DES_CU_OK if every group passed, T3DES_CU_ERR_ARG if one failed, or the
+ * error of a failing call. */
+int t3des_cu_run_verification(int device, char* report, size_t capacity);
+
 /* ---- contexts ------------------------------------------------------------ */
 
 int t3des_cu_device_count(int* count);

@@ -63,6 +63,7 @@ SIGNATURES = {
     "t3des_cu_triple_schedule": (_i, [_u64p, _u64p]),
     "t3des_cu_des_key_flags": (_i, [ctypes.c_uint64]),
     "t3des_cu_normalize_parity": (ctypes.c_uint64, [ctypes.c_uint64]),
+    "t3des_cu_run_verification": (_i, [_i, ctypes.c_char_p, _sz]),
     "t3des_cu_device_count": (_i, [ctypes.POINTER(_i)]),
     "t3des_cu_create": (_i, [_i, ctypes.POINTER(_vp)]),
     "t3des_cu_destroy": (_i, [_vp]),

@@ -471,6 +471,20 @@ tdes_encrypt_block_fast = tdes_encrypt_block  # tdes.hpp:53: the same function
 tdes_decrypt_block_fast = tdes_decrypt_block  # tdes.hpp:54
 
 
+def run_verification(out=None, device: int = 0) -> bool:
+    """verify.hpp:37: known answers and structural properties on the GPU
+    (t3des_cu_run_verification); writes the report to `out` (default
+    sys.stdout) and returns whether every group passed."""
+    import sys
+
+    buf = ctypes.create_string_buffer(4096)
+    rc = N.lib().t3des_cu_run_verification(device, buf, len(buf))
+    (out or sys.stdout).write(buf.value.decode())
+    if rc not in (N.OK, N.ERR_ARG):
+        _raise(rc)
+    return rc == N.OK
+
+
 class PaddingMode(enum.Enum):
     NONE = 0
     PKCS7 = 1

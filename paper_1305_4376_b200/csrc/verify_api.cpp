@@ -9,11 +9,15 @@
 // reference's (verify.cpp:65-124) — the walkthrough schedule, DES and 3DES
 // vectors, DES round trips and complementation, the EDE collapse — and
 // adds the NIST SP 800-67 three-block example as one batch.
+#include <algorithm>
 #include <cstdio>
+#include <cstring>
 #include <ostream>
 #include <random>
+#include <sstream>
 
 #include "t3des_b200/t3des.hpp"
+#include "t3des_cu.h"
 
 namespace t3des {
 namespace {
@@ -165,3 +169,26 @@ bool run_verification(std::ostream& out, const DispatchConfig& cfg) {
 }
 
 }  // namespace t3des
+
+extern "C" int t3des_cu_run_verification(int device, char* report, std::size_t capacity) {
+    std::ostringstream os;
+    int rc = T3DES_CU_OK;
+    try {
+        t3des::DispatchConfig cfg;
+        cfg.device = device;
+        if (!t3des::run_verification(os, cfg)) rc = T3DES_CU_ERR_ARG;
+    } catch (const t3des::CudaError& e) {
+        os << "error: " << e.what() << '\n';
+        rc = e.status;
+    } catch (const std::exception& e) {
+        os << "error: " << e.what() << '\n';
+        rc = T3DES_CU_ERR_ARG;
+    }
+    if (report && capacity) {
+        const std::string s = os.str();
+        const std::size_t n = std::min(s.size(), capacity - 1);
+        std::memcpy(report, s.data(), n);
+        report[n] = '\0';
+    }
+    return rc;
+}

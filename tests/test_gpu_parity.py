@@ -818,3 +818,8 @@ int main() {
     assert p.returncode == 0, (p.returncode, p.stdout, p.stderr)
     lines = p.stdout.strip().splitlines()
     assert lines[-1] == "verification PASSED" and len(lines) == 6 and all(l.startswith("ok") for l in lines[:-1])
+    import io
+
+    rep = io.StringIO()
+    assert t3.run_verification(rep) is True  # the Python mirror, through t3des_cu_run_verification
+    assert rep.getvalue().strip().splitlines() == lines
