@@ -1,0 +1,65 @@
+"""The reference's OWN unit tests against the B200 library.
+
+tests/native/refsuite/build.sh compiles /root/reference/proj/tests/
+test_des.cpp, test_tdes.cpp and test_dispatch.cpp — unchanged, where they
+lie — against include/t3des_b200/t3des.hpp and libt3des_b200.so, with a
+doctest stand-in (tests/native/refsuite/doctest.h) and forwarding headers
+for t3des/*.hpp.  The reference's two CPU backend names denote Backend::Cuda
+in that build (tests/native/refsuite/t3des/dispatch.hpp), so every batch,
+block and stream of the suite runs on the engine.  On a B200 every case must
+pass; without a device the host-only cases (schedules, key parsing and
+hygiene, plan_dispatch, PKCS#7, argument errors) pass and every device case
+fails loudly (no CPU fallback)."""
+import os
+import subprocess
+
+import pytest
+
+from tests.oracle_util import ROOT
+
+BUILD = os.path.join(ROOT, "tests", "native", "_build", "refsuite")
+SUITES = ["des", "tdes", "dispatch"]
+
+
+def run_suite(name: str):
+    exe = os.path.join(BUILD, f"test_{name}")
+    if not os.path.exists(exe):
+        pytest.skip("reference suites not built (no /root/reference at build time)")
+    p = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    cases = {}
+    for line in p.stdout.splitlines():
+        if line.startswith("[pass] ") or line.startswith("[FAIL] "):
+            name_part = line[7:].rsplit("  (", 1)[0]
+            cases[name_part] = (line.startswith("[pass]"), line)
+    return p, cases
+
+
+HOST_ONLY = {
+    "des": ["key schedule matches the independent walkthrough", "subkeys are 48 bits wide",
+            "schedule ignores parity bits", "all-zero key gives 16 identical subkeys",
+            "weak/semi-weak detection masks parity", "parity helpers", "block serialization is big-endian"],
+    "tdes": ["hex key parsing infers the keying option from length", "hex key parsing rejects bad input",
+             "option 2 and 3 schedules share passes", "to_hex round trips through the parser"],
+    "dispatch": ["plan_dispatch covers the input exactly", "plan_dispatch brute-force coverage",
+                 "partially overlapping buffers are rejected", "batch rejects ragged input",
+                 "PKCS#7 round trip for all lengths 0..64", "PKCS#7 unpad rejects malformed padding"],
+}
+
+
+@pytest.mark.parametrize("suite", SUITES)
+@pytest.mark.skipif("__import__('torch').cuda.is_available()")
+def test_reference_suite_host_cases_without_a_device(suite):
+    p, cases = run_suite(suite)
+    for name in HOST_ONLY[suite]:
+        assert cases.get(name, (False,))[0], (name, p.stdout[-3000:])
+    device_cases = [c for c in cases if c not in HOST_ONLY[suite]]
+    assert device_cases and all(not cases[c][0] for c in device_cases), p.stdout[-3000:]
+    assert p.returncode != 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("suite", SUITES)
+def test_reference_suite_passes_on_the_engine(suite):
+    p, cases = run_suite(suite)
+    assert p.returncode == 0 and cases and all(ok for ok, _ in cases.values()), (p.stdout[-4000:], p.stderr[-2000:])
+    assert len(cases) == {"des": 12, "tdes": 9, "dispatch": 18}[suite]
