@@ -13,10 +13,10 @@
 #include <cstring>
 #include <fstream>
 #include <iostream>
-#include <random>
 #include <string>
 #include <vector>
 
+#include "t3des_b200/bench.hpp"
 #include "t3des_b200/t3des.hpp"
 #include "t3des_cu.h"
 
@@ -194,19 +194,9 @@ int run_verify(const Opts& o) {
 }
 
 // ---- bench: GPU sweeps shaped like the reference's Tables I/II/IV ---------
-struct Rec {
-    unsigned workers;
-    std::size_t chunk, wg;
-    std::uint64_t bytes;
-    double secs = 0, mbs = 0, speedup = 0;
-    bool ok = true;
-};
-
-std::string fmt_double(double v) {
-    char b[32];
-    std::snprintf(b, sizeof b, "%.17g", v);
-    return b;
-}
+// Records, payload and reports are the library's t3des::bench (the reference
+// harness's interface and formats); the device mode times the kernels alone.
+using t3des::bench::BenchRecord;
 
 int run_bench(const Opts& o) {
     std::vector<std::size_t> values = o.values;
@@ -218,34 +208,32 @@ int run_bench(const Opts& o) {
     for (std::size_t i = 1; i < values.size(); ++i)
         if (values[i] <= values[i - 1]) throw UsageError("--values must be strictly increasing");
     const std::uint64_t bytes = o.payload_mb << 20;
-    std::vector<std::uint8_t> payload(bytes);
-    {
-        std::mt19937_64 rng(o.seed);  // reference make_payload layout (bench.cpp:41-51)
-        std::uint64_t w = 0;
-        for (std::uint64_t i = 0; i < bytes; ++i) {
-            if (i % 8 == 0) w = rng();
-            payload[i] = static_cast<std::uint8_t>(w >> (8 * (i % 8)));
-        }
-    }
+    const std::vector<std::uint8_t> payload = t3des::bench::make_payload(bytes, o.seed);
     const auto ts = t3des::triple_schedule(t3des::parse_hex_key("133457799BBCDFF10E329232EA6D0D737CA110454A1A6E57"));
     std::uint64_t sub48[48];
     std::memcpy(sub48, ts.pass1.data(), 128);
     std::memcpy(sub48 + 16, ts.pass2.data(), 128);
     std::memcpy(sub48 + 32, ts.pass3.data(), 128);
     std::vector<std::uint8_t> first_ct, out(bytes), back(bytes);
-    std::vector<Rec> recs;
+    std::vector<BenchRecord> recs;
     for (std::size_t v : values) {
-        Rec r{o.workers ? o.workers : 1, o.chunk_blocks, o.work_group, bytes};
+        BenchRecord r;
+        r.backend = t3des::Backend::Cuda;
+        r.workers = o.workers ? o.workers : 1;
+        r.chunk_blocks = o.chunk_blocks;
+        r.work_group = o.work_group;
+        r.payload_bytes = bytes;
         if (o.sweep == "workers") r.workers = static_cast<unsigned>(v);
-        if (o.sweep == "chunk") r.chunk = v;
-        if (o.sweep == "workgroup") r.wg = v;
-        const std::size_t wg_arg = r.wg;  // 0 = the kernels' own CTA-size rule
-        if (r.wg == 0) {  // report the size that rule picks (capi.cu launch_sptable / launch_bitslice)
-            const std::uint64_t launch_blocks = r.chunk ? std::min<std::uint64_t>(r.chunk, bytes / 8) : bytes / 8;
+        if (o.sweep == "chunk") r.chunk_blocks = v;
+        if (o.sweep == "workgroup") r.work_group = v;
+        const std::size_t wg_arg = r.work_group;  // 0 = the kernels' own CTA-size rule
+        if (r.work_group == 0) {  // report the size that rule picks (capi.cu launch_sptable / launch_bitslice)
+            const std::uint64_t launch_blocks =
+                r.chunk_blocks ? std::min<std::uint64_t>(r.chunk_blocks, bytes / 8) : bytes / 8;
             int sms = 148;
             if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, o.device) != cudaSuccess) sms = 148;
             const std::uint64_t per_sm = (launch_blocks + sms - 1) / std::uint64_t(sms);
-            r.wg = o.variant == "sptable" ? (per_sm >= 1024 ? 1024 : std::max<std::uint64_t>(128, (per_sm + 31) / 32 * 32))
+            r.work_group = o.variant == "sptable" ? (per_sm >= 1024 ? 1024 : std::max<std::uint64_t>(128, (per_sm + 31) / 32 * 32))
                                           : 128;
         }
         try {
@@ -269,7 +257,7 @@ int run_bench(const Opts& o) {
                     ck(cudaEventCreate(&e1))) {
                     rc = t3des_cu_set_schedule(c, sub48);
                     if (!rc) rc = t3des_cu_set_variant(c, make_config(o).variant);
-                    if (!rc) rc = t3des_cu_set_launch(c, r.chunk, static_cast<int>(wg_arg));
+                    if (!rc) rc = t3des_cu_set_launch(c, r.chunk_blocks, static_cast<int>(wg_arg));
                 }
                 for (unsigned rep = 0; rep <= o.reps && !rc; ++rep) {  // rep 0 = warm-up
                     ck(cudaEventRecord(e0, nullptr));
@@ -292,7 +280,7 @@ int run_bench(const Opts& o) {
             } else {
                 t3des::DispatchConfig cfg = make_config(o);
                 cfg.workers = r.workers;
-                cfg.chunk_blocks = r.chunk;
+                cfg.chunk_blocks = r.chunk_blocks;
                 cfg.work_group = wg_arg;
                 cfg.gpu_chunked = true;
                 for (unsigned rep = 0; rep <= o.reps; ++rep) {
@@ -309,8 +297,8 @@ int run_bench(const Opts& o) {
             if (back != payload) throw std::runtime_error("round trip mismatch");
             if (first_ct.empty()) first_ct = out;
             else if (out != first_ct) throw std::runtime_error("launch-shape dependence");
-            r.secs = best;
-            r.mbs = static_cast<double>(bytes) / best / (1 << 20);
+            r.compute_seconds = best;
+            r.throughput_mb_s = static_cast<double>(bytes) / best / (1 << 20);
         } catch (const std::exception& e) {
             std::cerr << "record failed: " << e.what() << '\n';
             r.ok = false;
@@ -318,30 +306,10 @@ int run_bench(const Opts& o) {
         recs.push_back(r);
     }
     if (!recs.empty() && recs[0].ok)
-        for (Rec& r : recs)
-            if (r.ok) r.speedup = recs[0].secs / r.secs;
-    std::string rep;
-    if (o.format == "csv") {
-        rep = "backend,workers,chunk_blocks,work_group,payload_bytes,compute_seconds,io_seconds,throughput_mb_s,"
-              "speedup_vs_baseline,ok\n";
-        for (const Rec& r : recs)
-            rep += "cuda," + std::to_string(r.workers) + "," + std::to_string(r.chunk) + "," + std::to_string(r.wg) +
-                   "," + std::to_string(r.bytes) + "," + fmt_double(r.secs) + ",0," + fmt_double(r.mbs) + "," +
-                   fmt_double(r.speedup) + "," + (r.ok ? "ok" : "failed") + "\n";
-    } else {
-        rep = "| backend | workers | chunk | work group | payload (B) | compute (s) | io (s) | MB/s | speedup |\n"
-              "|---|---|---|---|---|---|---|---|---|\n";
-        char b[256];
-        for (const Rec& r : recs) {
-            if (r.ok)
-                std::snprintf(b, sizeof b, "| cuda | %u | %zu | %zu | %llu | %.6f | %.4f | %.2f | %.2f |\n", r.workers,
-                              r.chunk, r.wg, (unsigned long long)r.bytes, r.secs, 0.0, r.mbs, r.speedup);
-            else
-                std::snprintf(b, sizeof b, "| cuda | %u | %zu | %zu | failed | - | - | - | - |\n", r.workers, r.chunk,
-                              r.wg);
-            rep += b;
-        }
-    }
+        for (BenchRecord& r : recs)
+            if (r.ok) r.speedup_vs_baseline = recs[0].compute_seconds / r.compute_seconds;
+    const std::string rep = t3des::bench::emit_report(
+        recs, o.format == "csv" ? t3des::bench::ReportFormat::Csv : t3des::bench::ReportFormat::Markdown);
     if (o.out.empty() || o.out == "-") {
         std::cout << rep;
     } else {
@@ -352,7 +320,7 @@ int run_bench(const Opts& o) {
         }
         f << rep;
     }
-    for (const Rec& r : recs)
+    for (const BenchRecord& r : recs)
         if (!r.ok) return kExitVerifyFailed;
     return 0;
 }

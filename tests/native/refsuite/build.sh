@@ -1,6 +1,6 @@
 #!/bin/bash
 # TEST INFRASTRUCTURE: compile the reference's OWN unit tests
-# (/root/reference/proj/tests/test_{des,tdes,dispatch}.cpp, where they lie —
+# (/root/reference/proj/tests/test_{des,tdes,dispatch,bench}.cpp, where they lie —
 # never copied into this repo) against the B200 library through its mirror
 # of the reference API (include/t3des_b200/t3des.hpp), with the doctest
 # stand-in and forwarding headers of this directory.  Outputs go to
@@ -14,8 +14,8 @@ OUT="$ROOT/tests/native/_build/refsuite"
 if [ ! -d "$REF/tests" ]; then echo "reference tree $REF absent: keeping prebuilt $OUT"; exit 0; fi
 mkdir -p "$OUT"
 LIB="$ROOT/paper_1305_4376_b200"
-for t in des tdes dispatch; do
+for t in des tdes dispatch bench; do
   /usr/bin/g++ -std=c++20 -O2 -DT3SHIM_MAIN -I"$HERE" -I"$ROOT/include" "$REF/tests/test_$t.cpp" \
     -L"$LIB" -lt3des_b200 -Wl,-rpath,"\$ORIGIN/../../../../paper_1305_4376_b200" -o "$OUT/test_$t"
 done
-echo "built $OUT/test_{des,tdes,dispatch}"
+echo "built $OUT/test_{des,tdes,dispatch,bench}"

@@ -3,18 +3,43 @@
 // ship it).  Enough of its interface to compile and run
 // /root/reference/proj/tests/test_{des,tdes,dispatch}.cpp unchanged against
 // the B200 library (tests/native/refsuite/build.sh): TEST_CASE, CHECK,
-// CHECK_FALSE, REQUIRE, CHECK_THROWS_AS, CAPTURE.  Each case runs in
+// CHECK_FALSE, REQUIRE, CHECK_THROWS_AS, CAPTURE, doctest::Approx.  Each case runs in
 // registration order; an exception escaping a case fails it; a failed
 // REQUIRE ends the case.  main() prints one line per case and a summary:
 //   [pass|FAIL] <case name>  (<failed checks>/<checks>)
 //   cases: P passed, F failed
 // and exits non-zero if any case failed.
 #pragma once
+#include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <exception>
 #include <functional>
 #include <string>
 #include <vector>
+
+namespace doctest {
+
+// doctest's relative comparison: |a - b| <= eps * (scale + max(|a|, |b|)),
+// default eps = 100 * float epsilon, scale 1.
+class Approx {
+  public:
+    explicit Approx(double v) : v_(v) {}
+    Approx& epsilon(double e) {
+        eps_ = e;
+        return *this;
+    }
+    friend bool operator==(double a, const Approx& b) {
+        return std::fabs(a - b.v_) <= b.eps_ * (1.0 + std::max(std::fabs(a), std::fabs(b.v_)));
+    }
+    friend bool operator==(const Approx& b, double a) { return a == b; }
+
+  private:
+    double v_;
+    double eps_ = 100 * 1.1920928955078125e-07;
+};
+
+}  // namespace doctest
 
 namespace t3shim {
 

@@ -1,12 +1,14 @@
 """The reference's OWN unit tests against the B200 library.
 
 tests/native/refsuite/build.sh compiles /root/reference/proj/tests/
-test_des.cpp, test_tdes.cpp and test_dispatch.cpp — unchanged, where they
+test_des.cpp, test_tdes.cpp, test_dispatch.cpp and test_bench.cpp — unchanged, where they
 lie — against include/t3des_b200/t3des.hpp and libt3des_b200.so, with a
 doctest stand-in (tests/native/refsuite/doctest.h) and forwarding headers
-for t3des/*.hpp.  The reference's two CPU backend names denote Backend::Cuda
-in that build (tests/native/refsuite/t3des/dispatch.hpp), so every batch,
-block and stream of the suite runs on the engine.  On a B200 every case must
+for t3des/*.hpp.  In the des/tdes/dispatch suites the reference's two CPU
+backend names denote Backend::Cuda (tests/native/refsuite/t3des/dispatch.hpp),
+so every batch, block and stream of those suites runs on the engine; the bench
+suite keeps the names (its records are report data) and its sweeps run on
+Backend::Cuda, the library's default.  On a B200 every case must
 pass; without a device the host-only cases (schedules, key parsing and
 hygiene, plan_dispatch, PKCS#7, argument errors) pass and every device case
 fails loudly (no CPU fallback)."""
@@ -18,7 +20,7 @@ import pytest
 from tests.oracle_util import ROOT
 
 BUILD = os.path.join(ROOT, "tests", "native", "_build", "refsuite")
-SUITES = ["des", "tdes", "dispatch"]
+SUITES = ["des", "tdes", "dispatch", "bench"]
 
 
 def run_suite(name: str):
@@ -43,6 +45,13 @@ HOST_ONLY = {
     "dispatch": ["plan_dispatch covers the input exactly", "plan_dispatch brute-force coverage",
                  "partially overlapping buffers are rejected", "batch rejects ragged input",
                  "PKCS#7 round trip for all lengths 0..64", "PKCS#7 unpad rejects malformed padding"],
+    # (without a device the harness's engine self-check fails, so the no-op
+    # backend's records are failed as the case expects)
+    "bench": ["speedup table from fixed times", "speedup table requires a baseline",
+              "empty record list emits a header-only CSV", "CSV round trip is exact",
+              "CSV parser rejects foreign input", "markdown report renders one row per record",
+              "sweep spec validation", "a failing backend is marked failed, sweep continues",
+              "payload generation is deterministic in the seed", "throughput uses compute time only"],
 }
 
 
@@ -62,4 +71,4 @@ def test_reference_suite_host_cases_without_a_device(suite):
 def test_reference_suite_passes_on_the_engine(suite):
     p, cases = run_suite(suite)
     assert p.returncode == 0 and cases and all(ok for ok, _ in cases.values()), (p.stdout[-4000:], p.stderr[-2000:])
-    assert len(cases) == {"des": 12, "tdes": 9, "dispatch": 18}[suite]
+    assert len(cases) == {"des": 12, "tdes": 9, "dispatch": 18, "bench": 12}[suite]
