@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <iterator>
 #include <cstdlib>
 #include <mutex>
 #include <thread>
@@ -32,11 +33,16 @@ std::vector<t3des_cu_ctx*> g_pool;  // idle contexts, any device
 
 int pool_acquire(int device, t3des_cu_ctx** out) {
     {
+        // most recently released first: a caller repeating one shape gets the
+        // contexts whose staging rings that shape already sized (handing out
+        // the least recently used instead rotated through every pooled
+        // context, and each one reallocated its ring for the new shard size:
+        // ~30 ms per call, scripts/workers_probe.cpp)
         std::lock_guard<std::mutex> lk(g_pool_mu);
-        for (auto it = g_pool.begin(); it != g_pool.end(); ++it)
+        for (auto it = g_pool.rbegin(); it != g_pool.rend(); ++it)
             if ((*it)->device == device) {
                 *out = *it;
-                g_pool.erase(it);
+                g_pool.erase(std::next(it).base());
                 return T3DES_CU_OK;
             }
     }

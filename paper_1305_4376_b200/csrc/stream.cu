@@ -81,7 +81,7 @@ std::size_t pkcs7_unpad_len(const std::uint8_t* data, std::size_t len) {
 }
 
 StreamStats run_stream(t3des_cu_ctx* c, int dir, ByteSource& src, ByteSink& dst, std::size_t chunk_blocks,
-                       bool pkcs7, std::size_t io_blocks) {
+                       bool pkcs7, std::size_t io_blocks, bool copy_only) {
     DeviceScope scope(c->device);  // the ring, staging and streams live on the context's device
     StreamStats st;
     const std::size_t logical = chunk_blocks * 8;  // the reference's chunk
@@ -90,7 +90,7 @@ StreamStats run_stream(t3des_cu_ctx* c, int dir, ByteSource& src, ByteSink& dst,
     const bool enc = dir == T3DES_CU_ENCRYPT;
     PinnedRing ring(chunk + 8);
     if (!ring.ok()) throw StreamFailure(StreamFailure::Cuda, "pinned staging allocation failed", 0, T3DES_CU_ERR_CUDA);
-    if (int rc = ensure_staging(c, chunk + 8, kSlots))
+    if (int rc = copy_only ? T3DES_CU_OK : ensure_staging(c, chunk + 8, kSlots))
         throw StreamFailure(StreamFailure::Cuda, t3des_cu_strerror(rc), 0, rc);
 
     std::deque<Slot> inflight;
@@ -200,7 +200,10 @@ StreamStats run_stream(t3des_cu_ctx* c, int dir, ByteSource& src, ByteSink& dst,
             }
             throw f;
         }
-        if (n) {
+        if (n && copy_only) {  // NoOpCopy: the slot is written out as read
+            inflight.push_back(Slot{slot, n, last});
+            ++st.chunks;
+        } else if (n) {
             auto t0 = Clock::now();
             cudaStream_t s = c->st[slot];
             std::uint8_t* d = c->buf[slot];

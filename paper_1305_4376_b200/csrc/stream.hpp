@@ -56,8 +56,10 @@ std::size_t pkcs7_unpad_len(const std::uint8_t* data, std::size_t len);
 // is read, transformed and written in: the output bytes, the padding and the
 // reported chunk count are those of chunk_blocks (the reference's chunks),
 // larger I/O only amortises per-call costs (the fd entry uses it for regular
-// files of known length).
+// files of known length).  copy_only: Backend::NoOpCopy (the reference's
+// timing instrument, dispatch.cpp:63-72) — the same chunking, padding, errors
+// and counters, with the chunks written out untransformed (no device work).
 StreamStats run_stream(t3des_cu_ctx* ctx, int direction, ByteSource& src, ByteSink& dst,
-                       std::size_t chunk_blocks, bool pkcs7, std::size_t io_blocks = 0);
+                       std::size_t chunk_blocks, bool pkcs7, std::size_t io_blocks = 0, bool copy_only = false);
 
 }  // namespace t3b

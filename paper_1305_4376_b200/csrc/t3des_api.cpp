@@ -106,8 +106,8 @@ struct OstreamSink : t3b::ByteSink {
 
 StreamReport run_stream(std::istream& source, std::ostream& sink, const TripleSchedule& ts,
                         const DispatchConfig& cfg, PaddingMode pad, int dir) {
-    if (cfg.backend != Backend::Cuda)
-        throw std::invalid_argument("t3des B200 engine: streams run on Backend::Cuda only");
+    if (cfg.backend != Backend::Cuda && cfg.backend != Backend::NoOpCopy)
+        throw std::invalid_argument("t3des B200 engine: streams run on Backend::Cuda (or NoOpCopy) only");
     if (cfg.chunk_blocks == 0) throw std::invalid_argument("chunk_blocks must be positive");
     std::uint64_t sub48[48];
     flatten(ts, sub48);
@@ -119,7 +119,8 @@ StreamReport run_stream(std::istream& source, std::ostream& sink, const TripleSc
     IstreamSource src(source);
     OstreamSink dst(sink);
     try {
-        const t3b::StreamStats s = t3b::run_stream(c, dir, src, dst, cfg.chunk_blocks, pad == PaddingMode::Pkcs7);
+        const t3b::StreamStats s = t3b::run_stream(c, dir, src, dst, cfg.chunk_blocks, pad == PaddingMode::Pkcs7, 0,
+                                                   cfg.backend == Backend::NoOpCopy);
         return StreamReport{s.bytes_in, s.bytes_out, s.chunks, s.compute_seconds, s.io_seconds};
     } catch (const t3b::StreamFailure& f) {
         switch (f.kind) {

@@ -1,6 +1,7 @@
 #!/bin/bash
 # TEST INFRASTRUCTURE: compile the reference's OWN unit tests
-# (/root/reference/proj/tests/test_{des,tdes,dispatch,bench}.cpp, where they lie —
+# (/root/reference/proj/tests/test_{des,tdes,dispatch,bench}.cpp and
+# acceptance.cpp, where they lie —
 # never copied into this repo) against the B200 library through its mirror
 # of the reference API (include/t3des_b200/t3des.hpp), with the doctest
 # stand-in and forwarding headers of this directory.  Outputs go to
@@ -18,4 +19,7 @@ for t in des tdes dispatch bench; do
   /usr/bin/g++ -std=c++20 -O2 -DT3SHIM_MAIN -I"$HERE" -I"$ROOT/include" "$REF/tests/test_$t.cpp" \
     -L"$LIB" -lt3des_b200 -Wl,-rpath,"\$ORIGIN/../../../../paper_1305_4376_b200" -o "$OUT/test_$t"
 done
-echo "built $OUT/test_{des,tdes,dispatch,bench}"
+# the reference's acceptance program (acceptance.cpp: one line per criterion)
+/usr/bin/g++ -std=c++20 -O2 -I"$HERE" -I"$ROOT/include" "$REF/tests/acceptance.cpp" \
+  -L"$LIB" -lt3des_b200 -Wl,-rpath,"\$ORIGIN/../../../../paper_1305_4376_b200" -o "$OUT/acceptance"
+echo "built $OUT/test_{des,tdes,dispatch,bench} and $OUT/acceptance"
