@@ -3,7 +3,9 @@
 // encrypt | decrypt | verify | bench, the same flags and the same exit codes
 // (0 ok, 1 I/O, 2 usage, 3 key format, 4 input length, 5 padding, 6 parity,
 // 7 verification failed).  Differences: the backend is "cuda" (the engine
-// has no CPU cipher), --workers counts GPUs, bench sweeps GPU launch shapes.
+// has no CPU cipher; the reference's names scalar/threaded run on the
+// engine, noop copies through), --workers counts GPUs, bench sweeps GPU
+// launch shapes.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -106,7 +108,13 @@ Opts parse(int argc, char** argv) {
     } else if (!pos.empty()) {
         throw UsageError("unexpected argument: " + pos[0]);
     }
-    if (o.backend != "cuda") throw UsageError("--backend must be cuda (the reference's CPU backends are not in this engine)");
+    // the reference's names are accepted so its scripts run unchanged:
+    // scalar/threaded (its two CPU routes of the same function) run on the
+    // engine, noop copies through as in the reference
+    if (o.backend != "cuda" && o.backend != "scalar" && o.backend != "threaded" && o.backend != "noop")
+        throw UsageError("--backend must be cuda|scalar|threaded|noop");
+    if ((o.backend == "scalar" || o.backend == "threaded") && crypt)
+        std::cerr << "note: --backend " << o.backend << " runs on the B200 engine (this build has no CPU cipher)\n";
     if (o.variant != "auto" && o.variant != "bitslice" && o.variant != "sptable")
         throw UsageError("--variant must be auto|bitslice|sptable");
     if (o.cmd == "bench") {
@@ -148,7 +156,7 @@ t3des::DispatchConfig make_config(const Opts& o) {
     cfg.workers = o.workers;
     if (cfg.workers == 0)
         if (const char* env = std::getenv("T3DES_WORKERS")) cfg.workers = static_cast<unsigned>(std::strtoul(env, nullptr, 10));
-    cfg.backend = t3des::Backend::Cuda;
+    cfg.backend = o.backend == "noop" ? t3des::Backend::NoOpCopy : t3des::Backend::Cuda;
     cfg.device = o.device;
     cfg.variant = o.variant == "sptable"    ? T3DES_CU_VARIANT_SPTABLE
                   : o.variant == "bitslice" ? T3DES_CU_VARIANT_BITSLICE
@@ -328,7 +336,8 @@ int run_bench(const Opts& o) {
 const char* kUsage =
     "usage: t3des_b200 <encrypt|decrypt> [--key HEX | --key-file F] [input|-] [output|-] [--pkcs7]\n"
     "                  [--check-parity] [--strict-keys] [--chunk-blocks N] [--work-group N]\n"
-    "                  [--workers N] [--backend cuda] [--variant auto|bitslice|sptable] [--device D]\n"
+    "                  [--workers N] [--backend cuda|scalar|threaded|noop] [--variant auto|bitslice|sptable]\n"
+    "                  [--device D]\n"
     "       t3des_b200 verify [--device D]\n"
     "       t3des_b200 bench [--sweep workers|chunk|workgroup] [--values a,b,...] [--payload-mb M]\n"
     "                  [--seed S] [--reps R] [--format csv|markdown] [--out F] [--mode device|host]\n";

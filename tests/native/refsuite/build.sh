@@ -22,4 +22,8 @@ done
 # the reference's acceptance program (acceptance.cpp: one line per criterion)
 /usr/bin/g++ -std=c++20 -O2 -I"$HERE" -I"$ROOT/include" "$REF/tests/acceptance.cpp" \
   -L"$LIB" -lt3des_b200 -Wl,-rpath,"\$ORIGIN/../../../../paper_1305_4376_b200" -o "$OUT/acceptance"
-echo "built $OUT/test_{des,tdes,dispatch,bench} and $OUT/acceptance"
+# the reference's CLI smoke script (tests/cli_smoke.cmake), staged next to
+# the binaries as a build output (git-ignored) for the GPU box, which has no
+# /root/reference; run with cmake -DCLI=<t3des_b200> -DWORKDIR=<dir> -P
+cp "$REF/tests/cli_smoke.cmake" "$OUT/cli_smoke.cmake"
+echo "built $OUT/test_{des,tdes,dispatch,bench} and $OUT/acceptance; staged cli_smoke.cmake"

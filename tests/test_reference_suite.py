@@ -94,3 +94,21 @@ def test_reference_acceptance_program_on_the_engine():
     assert set(lines) == set(range(1, 10)), p.stdout
     for c in (2, 3, 4, 8, 9):
         assert lines[c].startswith("PASS"), lines[c]
+
+
+@pytest.mark.gpu
+def test_reference_cli_smoke_script_on_our_cli(tmp_path):
+    """The reference's own CLI smoke test (tests/cli_smoke.cmake: round trip,
+    --backend scalar equivalence, PKCS#7, exit codes 2/3/4/6, key file,
+    verify, bench CSV) run with `cmake -P` against the t3des_b200 CLI."""
+    import shutil
+
+    script = os.path.join(BUILD, "cli_smoke.cmake")
+    cli = os.path.join(ROOT, "paper_1305_4376_b200", "t3des_b200")
+    if not os.path.exists(script):
+        pytest.skip("cli_smoke.cmake not staged (no /root/reference at build time)")
+    if not shutil.which("cmake"):
+        pytest.skip("cmake not installed")
+    p = subprocess.run(["cmake", f"-DCLI={cli}", f"-DWORKDIR={tmp_path}", "-P", script],
+                       capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0 and "cli smoke OK" in (p.stdout + p.stderr), (p.stdout[-3000:], p.stderr[-3000:])
