@@ -118,7 +118,7 @@ struct DispatchConfig {
                                         // whole batch per call (blocks per launch only
                                         // when gpu_chunked is set)
     std::size_t work_group = 256;       // CUDA: threads per CTA hint (used when gpu_chunked)
-    unsigned workers = 0;               // CUDA: block-range shards round-robin over the GPUs from `device` (0 = 1)
+    unsigned workers = 0;               // CUDA: block-range shards, at most one per GPU, from `device` (0 = 1)
     Backend backend = Backend::Cuda;
     int device = 0;                     // first CUDA device
     int variant = 6;                    // T3DES_CU_VARIANT_*: 6 auto (default), 0 bitsliced, 1 SP-table,

@@ -188,12 +188,14 @@ int t3des_cu_ecb_multi(const int* devices, int ndev, const uint64_t sub48[48], i
 
 /* The GPU reading of the reference's DispatchConfig.workers
  * (dispatch.hpp:28, the worker count its run_chunk hands to OpenMP,
- * dispatch.cpp:73-84): `workers` shards (0 = 1) of the host batch, assigned
- * round-robin to the visible devices starting at first_device — workers = 8
- * on an 8-GPU node uses every GPU once, workers = 2 on one GPU runs two
- * contexts on it.  workers <= 1 runs on a pooled context of first_device;
- * otherwise t3des_cu_ecb_multi over that device list.  Synchronous.  This is
- * what the patched reference's Backend::Cuda calls. */
+ * dispatch.cpp:73-84): min(workers, visible devices) shards (workers 0 = 1)
+ * of the host batch on consecutive devices from first_device (wrapping) —
+ * workers = 8 on an 8-GPU node uses every GPU once; on one GPU any workers
+ * value runs one shard (a CPU-sized thread count would only put several
+ * contexts on one device; t3des_cu_ecb_multi with a repeated device does
+ * that on purpose).  One shard runs on a pooled context of first_device;
+ * more go through t3des_cu_ecb_multi over that device list.  Synchronous.
+ * This is what the patched reference's Backend::Cuda calls. */
 int t3des_cu_ecb_workers(unsigned workers, int first_device, const uint64_t sub48[48], int direction,
                          const uint8_t* in, uint8_t* out, size_t len);
 

@@ -29,8 +29,8 @@ int main() {
         decrypt_batch(gpu, back, ts, c_gpu);
         if (back != in) { std::printf("decrypt mismatch n=%zu\n", n); return 1; }
     }
-    // cfg.workers > 1: that many block-range shards round-robin over the
-    // visible GPUs (workers = 2 on a one-GPU box: two contexts on it)
+    // cfg.workers > 1: min(workers, GPUs) block-range shards on consecutive
+    // GPUs (on a one-GPU box: one shard, whatever workers is)
     for (unsigned w : {2u, 3u}) {
         for (std::size_t n : {1ul, 2047ul, 100003ul, 3ul << 20}) {
             std::vector<std::uint8_t> in(8 * n), cpu(in.size()), gpu(in.size()), back(in.size());

@@ -188,7 +188,7 @@ class Backend(enum.Enum):
 class DispatchConfig:
     chunk_blocks: int = 131072  # blocks per launch, applied only if gpu_chunked
     work_group: int = 256       # threads per CTA, applied only if gpu_chunked
-    workers: int = 0            # CUDA: block-range shards, round-robin over the GPUs from `device` (0 = one)
+    workers: int = 0            # CUDA: block-range shards, at most one per GPU, from `device` (0 = one)
     backend: Backend = Backend.CUDA
     device: int = 0
     variant: int = N.VARIANT_AUTO
@@ -378,8 +378,8 @@ def _run_batch(src, dst, ts: TripleSchedule, cfg: DispatchConfig, direction: int
     if nin == 0:
         return
     if cfg.workers and cfg.workers > 1:
-        # workers shards round-robin over the visible GPUs from cfg.device
-        # (t3des_cu_ecb_workers; two on one GPU = two contexts on it)
+        # min(workers, GPUs) shards on consecutive GPUs from cfg.device
+        # (t3des_cu_ecb_workers)
         _raise(N.lib().t3des_cu_ecb_workers(cfg.workers, cfg.device, ts.sub48(), direction, pin, pout, nin))
         return
     e = engine(cfg.device)

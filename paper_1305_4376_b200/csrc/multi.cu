@@ -181,7 +181,13 @@ int t3des_cu_ecb_workers(unsigned workers, int first_device, const std::uint64_t
     }
     if (first_device < 0 || first_device >= n) return T3DES_CU_ERR_NO_DEVICE;
     if (!len) return T3DES_CU_OK;
-    const int w = workers == 0 ? 1 : int(workers);
+    // at most one shard per visible GPU: a reference caller sizes `workers`
+    // for CPU threads, and several contexts on one GPU only contend for its
+    // PCIe link and the host's copy threads (2 shards on one B200: 4.2 vs
+    // 2.7 ms for 64 MiB; 8 of them cost 0.6 s of context creation on first
+    // use; scripts/workers_probe.cpp).  t3des_cu_ecb_multi still takes any
+    // device list, repeated devices included.
+    const int w = workers == 0 ? 1 : int(std::min<unsigned>(workers, unsigned(n)));
     if (w == 1) {
         t3des_cu_ctx* c = nullptr;
         int rc = pool_acquire(first_device, &c);

@@ -70,7 +70,7 @@ void run_batch(std::span<const std::uint8_t> in, std::span<std::uint8_t> out, co
     std::uint64_t sub48[48];
     flatten(ts, sub48);
     int rc;
-    if (cfg.workers > 1) {  // shards round-robin over the visible GPUs from cfg.device
+    if (cfg.workers > 1) {  // min(workers, GPUs) shards on consecutive GPUs from cfg.device
         rc = t3des_cu_ecb_workers(cfg.workers, cfg.device, sub48, dir, ib, out.data(), in.size());
     } else {
         t3des_cu_ctx* c = context_for(cfg.device);
