@@ -64,10 +64,13 @@ extern "C" {
 /* Key-specialised bitsliced kernel: the installed schedule's
  * round keys folded into the LOP3 immediates of a cipher that NVRTC compiles
  * at run time, one module per (key sequence, direction), kept for the
- * process lifetime.  Opt-in, never chosen by AUTO: it executes the same ALU
- * operations per block as the table-driven kernel (whitening already keeps
- * the key XORs off the ALU pipe), and the first use of a key
- * pays the compile (t3des_cu_keyed_prepare; seconds).  Full 1024-block tiles
+ * process lifetime.  Opt-in: AUTO never compiles it — it executes about the
+ * same ALU operations per block as the table-driven kernel (whitening
+ * already keeps the key XORs off the ALU pipe) and the first use
+ * of a key pays the compile (t3des_cu_keyed_prepare; seconds) — but once
+ * t3des_cu_keyed_prepare has built it for the installed schedule and a
+ * direction, AUTO's bitsliced launches (> T3DES_CU_AUTO_SMALL_BLOCKS) in that
+ * direction run it, and small launches stay on the SP-table kernel.  Full 1024-block tiles
  * of 16-byte aligned spans run keyed; a partial tile and unaligned spans run
  * the table-driven kernels.  The compiled code embeds the key: it is held in
  * process and device memory only, never written to disk. */

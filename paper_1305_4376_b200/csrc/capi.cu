@@ -100,9 +100,13 @@ int launch_bitslice(t3des_cu_ctx* c, int dir, const std::uint8_t* in, std::uint8
                         : c->variant == T3DES_CU_VARIANT_BITSLICE_ALU ? 0
                         : c->variant == T3DES_CU_VARIANT_BITSLICE_DFMA ? T3_OPT_DFMA
                                                                        : T3_OPT_SHRFMA;
-        if (c->variant == T3DES_CU_VARIANT_KEYED && vec4) {
-            // key-specialised kernel (NVRTC, keyed.cpp); compiled on the first
-            // launch of a key unless t3des_cu_keyed_prepare ran
+        // key-specialised kernel (NVRTC, keyed.cpp): VARIANT_KEYED compiles it
+        // on the first launch of a key unless t3des_cu_keyed_prepare ran; AUTO
+        // takes it for its bitsliced launches once it has been prepared for the
+        // installed schedule and this direction (never compiles on its own)
+        const bool keyed = c->variant == T3DES_CU_VARIANT_KEYED ||
+                           (c->variant == T3DES_CU_VARIANT_AUTO && c->keyed[dir] != nullptr);
+        if (keyed && vec4) {
             if (int rc = t3b::keyed_launch(c, dir, in, out, full, s)) return rc;
         } else if (tma && c->rounds == 16 && opt == T3_OPT_DEFAULT_VALUE) {
             // collapsed EDE (K1 = K2 or K2 = K3): single DES, a third of the work

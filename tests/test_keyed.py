@@ -257,3 +257,56 @@ def test_keyed_variant_fuzz(keng, oracle):
                 got = _run(keng, key, src, direction).cpu().numpy()
             assert np.array_equal(got, oracle.ecb(x, s, direction)), (trial, key, n, direction, off)
             assert not buf[off + x.nbytes:].any()  # nothing written past the batch
+
+
+def _kernel_names(fn):
+    """Names of the CUDA kernels `fn` launches (torch.profiler / CUPTI sees
+    the engine library's launches too)."""
+    from torch.profiler import ProfilerActivity, profile
+
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        fn()
+        torch.cuda.synchronize()
+    return {e.name for e in prof.events()}
+
+
+@pytest.mark.gpu
+def test_auto_runs_a_prepared_keyed_module(keng, oracle):
+    """AUTO never compiles a keyed kernel, but once t3des_cu_keyed_prepare
+    has built one for the installed schedule and a direction, AUTO's
+    bitsliced launches in that direction run it (small launches stay on the
+    SP-table kernel, the other direction on the table-driven kernel), and a
+    new schedule drops it.  Bytes equal the oracle throughout."""
+    import paper_1305_4376_b200 as t3
+    from paper_1305_4376_b200 import _native as N
+
+    hexkey = KEYS["option1"]
+    s = oracle.schedule_hex(hexkey)
+    n = 1024 * 300 + 5  # > T3DES_CU_AUTO_SMALL_BLOCKS: bitsliced + side-stream tail
+    x = oracle.splitmix(0, n, 0xA070)
+    xd = torch.from_numpy(x).cuda()
+    out = torch.empty_like(xd)
+    st = torch.cuda.current_stream().cuda_stream
+    keng.set_schedule(t3.triple_schedule(t3.parse_hex_key(hexkey)))
+    keng.set_variant(N.VARIANT_AUTO)
+    keng.set_launch(0, 0)
+
+    def enc():
+        keng.ecb_device(0, xd.data_ptr(), out.data_ptr(), x.nbytes, st)
+
+    names = _kernel_names(enc)
+    assert not any("keyed" in k for k in names), names  # not prepared: table-driven
+    assert np.array_equal(out.cpu().numpy(), oracle.ecb(x, s, 0))
+    keng.keyed_prepare(0)
+    names = _kernel_names(enc)
+    assert any("t3_keyed_kernel" in k for k in names), names
+    assert np.array_equal(out.cpu().numpy(), oracle.ecb(x, s, 0))
+    back = torch.empty_like(xd)
+    names = _kernel_names(lambda: keng.ecb_device(1, out.data_ptr(), back.data_ptr(), x.nbytes, st))
+    assert not any("keyed" in k for k in names), names  # decrypt was not prepared
+    assert torch.equal(back, xd)
+    other = KEYS["option2"]
+    keng.set_schedule(t3.triple_schedule(t3.parse_hex_key(other)))
+    names = _kernel_names(enc)
+    assert not any("keyed" in k for k in names), names  # a new schedule drops it
+    assert np.array_equal(out.cpu().numpy(), oracle.ecb(x, oracle.schedule_hex(other), 0))
