@@ -549,10 +549,11 @@ def test_multi_device_chunk_pipeline(oracle, monkeypatch, chunk_bytes, n):
 
 @pytest.mark.parametrize("workers", [0, 1, 2, 3])
 def test_workers_axis(oracle, workers):
-    """t3des_cu_ecb_workers — DispatchConfig.workers on the GPU: that many
-    block-range shards round-robin over the visible GPUs (two or three
-    contexts on one GPU here), pageable and pinned spans; the Python API
-    routes cfg.workers > 1 through it."""
+    """t3des_cu_ecb_workers — DispatchConfig.workers on the GPU:
+    min(workers, GPUs) block-range shards on consecutive GPUs (one shard on a
+    one-GPU box, whatever workers is), pageable and pinned spans; the Python
+    API routes cfg.workers > 1 through it.  Several contexts on one device
+    are exercised through t3des_cu_ecb_multi (test_multi_device_api_shards)."""
     s = oracle.schedule_hex(KEYS[0])
     x = oracle.payload(8 * (5 * 1024 * 7 + 3))
     y = np.empty_like(x)
